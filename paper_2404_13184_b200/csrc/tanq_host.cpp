@@ -1,0 +1,1550 @@
+// libtanq host side: C ABI (include/tanq.h), superoperator builder, noise binding, gate
+// fusion, layout / remap planner and device orchestration.  Kernels: tanq_kernels.cu.
+//
+// Citations: P:n = /root/reference/PAPER.md line n.  DESIGN.md lists the readings R1-R20.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "tanq.h"
+#include "tanq_internal.h"
+
+using cd = std::complex<double>;
+
+namespace {
+
+thread_local std::string g_err;
+
+tanq_status fail(tanq_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+// NCCL is loaded on demand (multi-process mode only) with dlopen: an already-loaded
+// libnccl.so.2 (e.g. the one torch brought in) is reused, so the library never pins an
+// NCCL version into a process that imports torch afterwards.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) {
+    const char* env = getenv("TANQ_NCCL_LIB");
+    h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) return api;
+#define LOAD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+  LOAD(GetUniqueId);
+  LOAD(CommInitRank);
+  LOAD(CommDestroy);
+  LOAD(GroupStart);
+  LOAD(GroupEnd);
+  LOAD(Send);
+  LOAD(Recv);
+  LOAD(AllReduce);
+  LOAD(GetErrorString);
+#undef LOAD
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart &&
+           api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.GetErrorString;
+  return api;
+}
+
+#define CUDA_TRY(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t _e = (x);                                                               \
+    if (_e != cudaSuccess)                                                              \
+      return fail(TANQ_E_CUDA, std::string(#x) + " -> " + cudaGetErrorString(_e));     \
+  } while (0)
+#define NCCL_TRY(x)                                                                     \
+  do {                                                                                  \
+    ncclResult_t _r = (x);                                                              \
+    if (_r != ncclSuccess)                                                              \
+      return fail(TANQ_E_NCCL, std::string(#x) + " -> " + nccl().GetErrorString(_r));    \
+  } while (0)
+#define TRY(x)                                                                          \
+  do {                                                                                  \
+    tanq_status _s = (x);                                                               \
+    if (_s != TANQ_OK) return _s;                                                       \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// small dense complex matrices (row-major)
+// ------------------------------------------------------------------------------------
+struct Mat {
+  int d = 0;
+  std::vector<cd> a;
+  Mat() = default;
+  explicit Mat(int dim) : d(dim), a((size_t)dim * dim, cd(0.0, 0.0)) {}
+  cd& operator()(int i, int j) { return a[(size_t)i * d + j]; }
+  const cd& operator()(int i, int j) const { return a[(size_t)i * d + j]; }
+};
+
+Mat identity(int d) {
+  Mat m(d);
+  for (int i = 0; i < d; ++i) m(i, i) = 1.0;
+  return m;
+}
+
+Mat matmul(const Mat& A, const Mat& B) {
+  Mat C(A.d);
+  for (int i = 0; i < A.d; ++i)
+    for (int l = 0; l < A.d; ++l) {
+      const cd x = A(i, l);
+      if (x == cd(0.0, 0.0)) continue;
+      for (int j = 0; j < A.d; ++j) C(i, j) += x * B(l, j);
+    }
+  return C;
+}
+
+// ------------------------------------------------------------------------------------
+// gate unitaries (local index sum_j b(q_j) 2^j; q[0] = control of CX/CZ/CP)
+// ------------------------------------------------------------------------------------
+int kind_arity(int kind) {
+  if (kind >= TANQ_ID && kind <= TANQ_RZ) return 1;
+  if (kind >= TANQ_CX && kind <= TANQ_SWAP) return 2;
+  return 0;  // user matrices: arity from op.k
+}
+
+Mat gate_unitary(int kind, double th) {
+  const double c = std::cos(th / 2), s = std::sin(th / 2), r2 = 1.0 / std::sqrt(2.0);
+  const cd I(0.0, 1.0);
+  Mat u(kind_arity(kind) == 2 ? 4 : 2);
+  switch (kind) {
+    case TANQ_ID: u = identity(2); break;
+    case TANQ_X: u(0, 1) = 1; u(1, 0) = 1; break;
+    case TANQ_Y: u(0, 1) = -I; u(1, 0) = I; break;
+    case TANQ_Z: u(0, 0) = 1; u(1, 1) = -1; break;
+    case TANQ_H: u(0, 0) = r2; u(0, 1) = r2; u(1, 0) = r2; u(1, 1) = -r2; break;
+    case TANQ_S: u(0, 0) = 1; u(1, 1) = I; break;
+    case TANQ_SDG: u(0, 0) = 1; u(1, 1) = -I; break;
+    case TANQ_T: u(0, 0) = 1; u(1, 1) = std::polar(1.0, M_PI / 4); break;
+    case TANQ_TDG: u(0, 0) = 1; u(1, 1) = std::polar(1.0, -M_PI / 4); break;
+    case TANQ_SX:
+      u(0, 0) = cd(0.5, 0.5); u(0, 1) = cd(0.5, -0.5);
+      u(1, 0) = cd(0.5, -0.5); u(1, 1) = cd(0.5, 0.5);
+      break;
+    case TANQ_RX: u(0, 0) = c; u(0, 1) = -I * s; u(1, 0) = -I * s; u(1, 1) = c; break;
+    case TANQ_RY: u(0, 0) = c; u(0, 1) = -s; u(1, 0) = s; u(1, 1) = c; break;
+    case TANQ_RZ: u(0, 0) = std::polar(1.0, -th / 2); u(1, 1) = std::polar(1.0, th / 2); break;
+    case TANQ_CX:  // |c=1,t=0> (1) <-> |c=1,t=1> (3)
+      u(0, 0) = 1; u(2, 2) = 1; u(3, 1) = 1; u(1, 3) = 1;
+      break;
+    case TANQ_CZ: u(0, 0) = 1; u(1, 1) = 1; u(2, 2) = 1; u(3, 3) = -1; break;
+    case TANQ_CP: u(0, 0) = 1; u(1, 1) = 1; u(2, 2) = 1; u(3, 3) = std::polar(1.0, th); break;
+    case TANQ_SWAP: u(0, 0) = 1; u(1, 2) = 1; u(2, 1) = 1; u(3, 3) = 1; break;
+  }
+  return u;
+}
+
+// ------------------------------------------------------------------------------------
+// superoperators, local vec index l = r + c d (column stacking)
+// ------------------------------------------------------------------------------------
+// vec(U X U^dag)[r' + c' d] = sum U[r'][r] X[r][c] conj(U[c'][c])  ->  S = conj(U) (x) U
+void add_superop_of(const Mat& K, Mat& S) {
+  const int d = K.d;
+  for (int c2 = 0; c2 < d; ++c2)
+    for (int r2 = 0; r2 < d; ++r2)
+      for (int c = 0; c < d; ++c) {
+        const cd kc = std::conj(K(c2, c));
+        if (kc == cd(0.0, 0.0)) continue;
+        for (int r = 0; r < d; ++r) S(r2 + c2 * d, r + c * d) += kc * K(r2, r);
+      }
+}
+
+Mat superop_from_kraus(const std::vector<Mat>& Ks) {
+  Mat S(Ks[0].d * Ks[0].d);
+  for (const Mat& K : Ks) add_superop_of(K, S);
+  return S;
+}
+
+// depolarizing on the k qubits jointly (reading R7): (1-p) X + p tr(X) I/d
+Mat superop_depol(int k, double p) {
+  const int d = 1 << k, D = d * d;
+  Mat S = identity(D);
+  for (int i = 0; i < D; ++i) S(i, i) *= (1.0 - p);
+  for (int r = 0; r < d; ++r)
+    for (int r2 = 0; r2 < d; ++r2) S(r2 + r2 * d, r + r * d) += p / d;
+  return S;
+}
+
+// thermal relaxation on one qubit (reading R8): populations rho11 -> e^{-t/T1} rho11,
+// rho00 -> rho00 + (1 - e^{-t/T1}) rho11, coherences -> e^{-t/T2}.  (AD(gamma) then
+// PD(lambda) with gamma = 1 - e^{-t/T1}, lambda = 1 - e^{-2t(1/T2 - 1/(2T1))}.)
+Mat superop_thermal(double t1, double t2, double t) {
+  Mat S(4);
+  const double e1 = std::exp(-t / t1), e2 = std::exp(-t / t2);
+  S(0, 0) = 1.0;
+  S(0, 3) = 1.0 - e1;
+  S(3, 3) = e1;
+  S(1, 1) = e2;
+  S(2, 2) = e2;
+  return S;
+}
+
+// coherent over-rotation (reading R10): E = cos(e/2) I - i sin(e/2) A, A^2 = I
+Mat overrot_unitary(int k, double eps) {
+  const int d = 1 << k;
+  Mat A(d);
+  if (k == 1) {
+    A(0, 1) = 1; A(1, 0) = 1;
+  } else {  // Z on local qubit 0 (control), X on local qubit 1 (target)
+    for (int i = 0; i < 4; ++i) {
+      int j = i ^ 2;
+      A(j, i) = (i & 1) ? -1.0 : 1.0;
+    }
+  }
+  Mat E(d);
+  const double c = std::cos(eps / 2), s = std::sin(eps / 2);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) E(i, j) = (i == j ? c : 0.0) + cd(0.0, -s) * A(i, j);
+  return E;
+}
+
+// Embed a superoperator on sub-qubits (positions pos[j] within a k-qubit local space).
+Mat embed_superop(const Mat& Ss, const std::vector<int>& pos, int k) {
+  const int ks = (int)pos.size(), ds = 1 << ks, d = 1 << k, D = d * d;
+  if (ks == k) {
+    bool ident = true;
+    for (int j = 0; j < k; ++j) ident &= pos[j] == j;
+    if (ident) return Ss;
+  }
+  int mask = 0;
+  for (int p : pos) mask |= 1 << p;
+  auto sub = [&](int x) {
+    int v = 0;
+    for (int j = 0; j < ks; ++j) v |= ((x >> pos[j]) & 1) << j;
+    return v;
+  };
+  Mat S(D);
+  for (int l2 = 0; l2 < D; ++l2) {
+    const int r2 = l2 & (d - 1), c2 = l2 >> k;
+    for (int l = 0; l < D; ++l) {
+      const int r = l & (d - 1), c = l >> k;
+      if ((r2 & ~mask) != (r & ~mask) || (c2 & ~mask) != (c & ~mask)) continue;
+      S(l2, l) = Ss(sub(r2) + sub(c2) * ds, sub(r) + sub(c) * ds);
+    }
+  }
+  return S;
+}
+
+// ------------------------------------------------------------------------------------
+// ops, fusion
+// ------------------------------------------------------------------------------------
+struct FusedOp {
+  int k = 0;
+  int q[3] = {0, 0, 0};
+  Mat S;            // 4^k, local index over q[0..k-1]
+  int parts = 1;    // number of pre-fusion ops folded in
+};
+
+// B200 cost of one op in units of one HBM read+write pass (32 B / amplitude), DESIGN.md
+// §Fusion cost model: k<=2 FMA ops hide their FP64 work under the pass; a dense k=3 op on
+// DMMA with the 3-multiply complex product costs 192 FMA/amplitude / (FP64 rate) ~ 2.1.
+double op_cost(int k) { return k <= 2 ? 1.0 : 2.1; }
+
+bool shares(const FusedOp& a, const int* q, int k) {
+  for (int i = 0; i < a.k; ++i)
+    for (int j = 0; j < k; ++j)
+      if (a.q[i] == q[j]) return true;
+  return false;
+}
+
+// Fold G into Q (G applied after Q) on the union of their qubits.
+FusedOp merge(const FusedOp& Q, const FusedOp& G) {
+  FusedOp U;
+  U.k = Q.k;
+  for (int i = 0; i < Q.k; ++i) U.q[i] = Q.q[i];
+  for (int j = 0; j < G.k; ++j) {
+    bool found = false;
+    for (int i = 0; i < U.k; ++i) found |= U.q[i] == G.q[j];
+    if (!found) U.q[U.k++] = G.q[j];
+  }
+  std::vector<int> pq, pg;
+  for (int i = 0; i < Q.k; ++i) pq.push_back(i);
+  for (int j = 0; j < G.k; ++j)
+    for (int i = 0; i < U.k; ++i)
+      if (U.q[i] == G.q[j]) pg.push_back(i);
+  U.S = matmul(embed_superop(G.S, pg, U.k), embed_superop(Q.S, pq, U.k));
+  U.parts = Q.parts + G.parts;
+  return U;
+}
+
+// mode 1: paper -- merge into the latest op touching the same qubits only if it
+// acts on the identical ordered qubit tuple.  mode 2: greedy union up to k_max (<= 2 first,
+// then 3-qubit groups kept only when the cost model says they save passes).
+std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
+  if (mode == 0) return in;
+  auto pass = [&](const std::vector<FusedOp>& src, int klim, bool paper) {
+    std::vector<FusedOp> out;
+    out.reserve(src.size());
+    for (const FusedOp& G : src) {
+      int idx = -1;
+      for (int i = (int)out.size() - 1; i >= 0; --i)
+        if (shares(out[i], G.q, G.k)) {
+          idx = i;
+          break;
+        }
+      if (idx >= 0) {
+        FusedOp& Q = out[idx];
+        if (paper) {
+          bool same = Q.k == G.k;
+          for (int i = 0; same && i < G.k; ++i) same = Q.q[i] == G.q[i];
+          if (same) {
+            Q.S = matmul(G.S, Q.S);
+            Q.parts += G.parts;
+            continue;
+          }
+        } else {
+          int uk = Q.k;
+          for (int j = 0; j < G.k; ++j) {
+            bool f = false;
+            for (int i = 0; i < Q.k; ++i) f |= Q.q[i] == G.q[j];
+            if (!f) ++uk;
+          }
+          if (uk <= klim && op_cost(uk) <= op_cost(Q.k) + op_cost(G.k)) {
+            Q = merge(Q, G);
+            continue;
+          }
+        }
+      }
+      out.push_back(G);
+    }
+    return out;
+  };
+  if (mode == 1) return pass(in, 2, true);
+  std::vector<FusedOp> l1 = pass(in, std::min(kmax, 2), false);
+  if (kmax < 3) return l1;
+  // 3-qubit grouping: greedy groups of <= 3 qubits over the k<=2 ops; a group replaces its
+  // members only when their summed pass cost exceeds one dense k=3 pass.
+  struct Group {
+    FusedOp op;
+    std::vector<int> members;
+  };
+  std::vector<Group> groups;
+  for (int gi = 0; gi < (int)l1.size(); ++gi) {
+    const FusedOp& G = l1[gi];
+    int idx = -1;
+    for (int i = (int)groups.size() - 1; i >= 0; --i)
+      if (shares(groups[i].op, G.q, G.k)) {
+        idx = i;
+        break;
+      }
+    if (idx >= 0) {
+      Group& Q = groups[idx];
+      int uk = Q.op.k;
+      for (int j = 0; j < G.k; ++j) {
+        bool f = false;
+        for (int i = 0; i < Q.op.k; ++i) f |= Q.op.q[i] == G.q[j];
+        if (!f) ++uk;
+      }
+      if (uk <= 3) {
+        Q.op = merge(Q.op, G);
+        Q.members.push_back(gi);
+        continue;
+      }
+    }
+    groups.push_back(Group{G, {gi}});
+  }
+  std::vector<FusedOp> out;
+  for (Group& g : groups) {
+    double sep = 0;
+    for (int m : g.members) sep += op_cost(l1[m].k);
+    if (g.op.k == 3 && op_cost(3) < sep) {
+      out.push_back(g.op);
+    } else {
+      for (int m : g.members) out.push_back(l1[m]);
+    }
+  }
+  return out;
+}
+
+struct Prof {
+  int cls;
+  cudaEvent_t e0, e1;
+  double bytes, flops;
+};
+const char* kProfNames[] = {"gate_k1", "gate_k2", "gate_k3_dmma", "remap"};
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// the simulator handle
+// ------------------------------------------------------------------------------------
+struct Shard {
+  int id = 0;          // global shard id
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double2* data = nullptr;
+};
+
+struct DevScratch {
+  int device = -1;
+  double* probs = nullptr;        // 2^n
+  double* probs_tmp = nullptr;    // 2^n (multi-device combine)
+  double* cdf = nullptr;          // 2^n
+  double2* partial = nullptr;     // expect partial sums
+  double2* scal = nullptr;        // 2 double2
+  unsigned long long* imax = nullptr;
+  double2* stage = nullptr;       // get/set_state staging
+  size_t stage_elems = 0;
+  double2* frag = nullptr;        // k=3 fragment buffer
+  size_t frag_elems = 0;
+};
+
+struct tanq_sim {
+  int n = 0, L = 0, world = 1, rank0 = 0;
+  bool dist = false;
+  std::vector<Shard> shards;
+  std::vector<DevScratch> scratch;  // per distinct device
+  uint32_t phys[64];                // logical bit (2q row, 2q+1 col) -> physical bit
+  ncclComm_t comm = nullptr;
+  double2* xsend = nullptr;
+  double2* xrecv = nullptr;
+  size_t xchunk = 0;
+  bool prof_on = false;
+  std::vector<Prof> prof;
+  double prof_ms[4] = {0, 0, 0, 0};
+  double prof_bytes[4] = {0, 0, 0, 0};
+  double prof_flops[4] = {0, 0, 0, 0};
+  uint64_t prof_launches[4] = {0, 0, 0, 0};
+  uint64_t launches = 0;
+  uint64_t remap_count = 0, remap_bytes = 0;
+  std::vector<std::pair<int, cudaStream_t>> owned;  // library-created stream per device
+  cudaStream_t own_streams_of(int dev) const {
+    for (auto& p : owned)
+      if (p.first == dev) return p.second;
+    return nullptr;
+  }
+};
+
+namespace {
+
+DevScratch& scratch_for(tanq_sim* s, int device) {
+  for (auto& d : s->scratch)
+    if (d.device == device) return d;
+  s->scratch.push_back(DevScratch{});
+  s->scratch.back().device = device;
+  return s->scratch.back();
+}
+
+tanq_status ensure_scratch(tanq_sim* s, DevScratch& d) {
+  if (d.probs) return TANQ_OK;
+  CUDA_TRY(cudaSetDevice(d.device));
+  const size_t N = (size_t)1 << s->n;
+  CUDA_TRY(cudaMalloc(&d.probs, N * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&d.probs_tmp, N * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&d.cdf, N * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&d.partial, 148 * 4 * sizeof(double2)));
+  CUDA_TRY(cudaMalloc(&d.scal, 2 * sizeof(double2)));
+  CUDA_TRY(cudaMalloc(&d.imax, sizeof(unsigned long long)));
+  d.stage_elems = (size_t)1 << 21;  // 32 MiB
+  CUDA_TRY(cudaMalloc(&d.stage, d.stage_elems * sizeof(double2)));
+  return TANQ_OK;
+}
+
+tanq::BitMap bitmap_of(const tanq_sim* s) {
+  tanq::BitMap bm;
+  bm.nbits = 2 * s->n;
+  for (int i = 0; i < 64; ++i) bm.phys[i] = s->phys[i];
+  return bm;
+}
+
+void reset_layout(tanq_sim* s) {
+  for (int i = 0; i < 64; ++i) s->phys[i] = (uint32_t)i;  // rowpos(q)=2q, colpos(q)=2q+1
+}
+
+// wait for all shards' streams (cross-stream / cross-device ordering point)
+tanq_status join_all(tanq_sim* s) {
+  for (auto& sh : s->shards) {
+    CUDA_TRY(cudaSetDevice(sh.device));
+    CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  }
+  return TANQ_OK;
+}
+
+tanq_status stream_wait(const Shard& waiter, const Shard& on) {
+  if (waiter.stream == on.stream) return TANQ_OK;
+  cudaEvent_t ev;
+  CUDA_TRY(cudaSetDevice(on.device));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev, on.stream));
+  CUDA_TRY(cudaSetDevice(waiter.device));
+  CUDA_TRY(cudaStreamWaitEvent(waiter.stream, ev, 0));
+  CUDA_TRY(cudaEventDestroy(ev));
+  return TANQ_OK;
+}
+
+// Swap physical bit a (global, a >= L) with local bit b (A-6).
+tanq_status remap_swap(tanq_sim* s, int a, int b) {
+  const int L = s->L, gb = a - L;
+  const uint64_t half = (uint64_t)1 << (L - 1);
+  if (!s->dist) {
+    for (auto& sh : s->shards) {
+      const int g = sh.id;
+      if ((g >> gb) & 1) continue;
+      const int g2 = g ^ (1 << gb);
+      Shard* other = nullptr;
+      for (auto& o : s->shards)
+        if (o.id == g2) other = &o;
+      TRY(stream_wait(sh, *other));
+      CUDA_TRY(cudaSetDevice(sh.device));
+      const int va = 1 - ((g >> gb) & 1), vb = 1 - ((g2 >> gb) & 1);
+      CUDA_TRY(tanq::launch_swap_halves(sh.data, other->data, L, b, va, vb, sh.stream));
+      s->launches++;
+      TRY(stream_wait(*other, sh));
+      s->remap_bytes += half * sizeof(double2);
+    }
+  } else {
+    Shard& sh = s->shards[0];
+    const int g = sh.id, g2 = g ^ (1 << gb);
+    const int v = 1 - ((g >> gb) & 1);
+    CUDA_TRY(cudaSetDevice(sh.device));
+    for (uint64_t first = 0; first < half; first += s->xchunk) {
+      const uint64_t cnt = std::min<uint64_t>(s->xchunk, half - first);
+      CUDA_TRY(tanq::launch_pack_half(sh.data, s->xsend, b, v, first, cnt, sh.stream));
+      NCCL_TRY(nccl().GroupStart());
+      NCCL_TRY(nccl().Send(s->xsend, cnt * 2, ncclDouble, g2, s->comm, sh.stream));
+      NCCL_TRY(nccl().Recv(s->xrecv, cnt * 2, ncclDouble, g2, s->comm, sh.stream));
+      NCCL_TRY(nccl().GroupEnd());
+      CUDA_TRY(tanq::launch_unpack_half(sh.data, s->xrecv, b, v, first, cnt, sh.stream));
+      s->launches += 2;
+      s->remap_bytes += cnt * sizeof(double2);
+    }
+  }
+  // bookkeeping: logical bits at a and b exchange positions
+  for (int i = 0; i < 2 * s->n; ++i) {
+    if (s->phys[i] == (uint32_t)a)
+      s->phys[i] = (uint32_t)b;
+    else if (s->phys[i] == (uint32_t)b)
+      s->phys[i] = (uint32_t)a;
+  }
+  s->remap_count++;
+  return TANQ_OK;
+}
+
+// Make every target bit of (k, q) local; victims = local bits not targeted, whose qubit is
+// used furthest in the future (lookahead over `next`), ties to the highest position.
+tanq_status ensure_local(tanq_sim* s, int k, const int* q, const std::vector<FusedOp>* next,
+                         size_t next_from) {
+  const int L = s->L;
+  std::vector<int> tgt;
+  for (int j = 0; j < k; ++j) {
+    tgt.push_back(2 * q[j]);
+    tgt.push_back(2 * q[j] + 1);
+  }
+  for (int id : tgt) {
+    const int a = (int)s->phys[id];
+    if (a < L) continue;
+    int best = -1;
+    long best_dist = -1;
+    for (int b = L - 1; b >= 0; --b) {
+      int lid = -1;
+      for (int i = 0; i < 2 * s->n; ++i)
+        if (s->phys[i] == (uint32_t)b) lid = i;
+      if (std::find(tgt.begin(), tgt.end(), lid) != tgt.end()) continue;
+      const int lq = lid / 2;
+      long dist = 1L << 40;
+      if (next) {
+        for (size_t t = next_from; t < next->size() && t < next_from + 256; ++t) {
+          const FusedOp& f = (*next)[t];
+          bool uses = false;
+          for (int j = 0; j < f.k; ++j) uses |= f.q[j] == lq;
+          if (uses) {
+            dist = (long)(t - next_from);
+            break;
+          }
+        }
+      }
+      if (dist > best_dist) {
+        best_dist = dist;
+        best = b;
+      }
+    }
+    if (best < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
+    TRY(remap_swap(s, a, best));
+  }
+  return TANQ_OK;
+}
+
+void prof_begin(tanq_sim* s, Shard& sh, Prof& p) {
+  if (!s->prof_on || sh.id != s->rank0) return;
+  cudaEventCreate(&p.e0);
+  cudaEventCreate(&p.e1);
+  cudaEventRecord(p.e0, sh.stream);
+}
+void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
+  if (!s->prof_on || sh.id != s->rank0) return;
+  cudaEventRecord(p.e1, sh.stream);
+  s->prof.push_back(p);
+}
+
+tanq_status prof_flush(tanq_sim* s) {
+  if (s->prof.empty()) return TANQ_OK;
+  TRY(join_all(s));
+  for (Prof& p : s->prof) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.e0, p.e1);
+    s->prof_ms[p.cls] += ms;
+    s->prof_bytes[p.cls] += p.bytes;
+    s->prof_flops[p.cls] += p.flops;
+    s->prof_launches[p.cls]++;
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  s->prof.clear();
+  return TANQ_OK;
+}
+
+// Launch one fused op on every shard (targets must be local).  frag3: device fragment
+// buffer per device for k = 3 (indexed like s->scratch).
+tanq_status launch_op(tanq_sim* s, const FusedOp& op, const std::vector<const double2*>* frag3) {
+  const int k = op.k, M = 1 << (2 * k);
+  // sorted physical target positions; member bit t <-> pos[t]
+  std::vector<std::pair<int, int>> bits;  // (phys pos, local-vec bit: r_j -> j, c_j -> k + j)
+  for (int j = 0; j < k; ++j) {
+    bits.push_back({(int)s->phys[2 * op.q[j]], j});
+    bits.push_back({(int)s->phys[2 * op.q[j] + 1], k + j});
+  }
+  std::sort(bits.begin(), bits.end());
+  std::vector<int> l_of(M);
+  for (int i = 0; i < M; ++i) {
+    int l = 0;
+    for (int t = 0; t < 2 * k; ++t)
+      if ((i >> t) & 1) l |= 1 << bits[t].second;
+    l_of[i] = l;
+  }
+  const uint64_t n_tuples = (uint64_t)1 << (s->L - 2 * k);
+  const double amps = (double)((uint64_t)1 << s->L);
+  for (auto& sh : s->shards) {
+    CUDA_TRY(cudaSetDevice(sh.device));
+    Prof pr{k - 1, nullptr, nullptr, 32.0 * amps, 8.0 * M * amps};
+    prof_begin(s, sh, pr);
+    if (k == 1 || k == 2) {
+      if (k == 1) {
+        tanq::GateParams<1> p;
+        for (int i = 0; i < M; ++i)
+          for (int j = 0; j < M; ++j) {
+            cd v = op.S(l_of[i], l_of[j]);
+            p.S[i * M + j] = make_double2(v.real(), v.imag());
+          }
+        for (int t = 0; t < 2; ++t) {
+          p.pos[t] = (uint32_t)bits[t].first;
+          p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
+        }
+        p.n_tuples = n_tuples;
+        CUDA_TRY(tanq::launch_gate1(sh.data, p, sh.stream));
+      } else {
+        tanq::GateParams<2> p;
+        for (int i = 0; i < M; ++i)
+          for (int j = 0; j < M; ++j) {
+            cd v = op.S(l_of[i], l_of[j]);
+            p.S[i * M + j] = make_double2(v.real(), v.imag());
+          }
+        for (int t = 0; t < 4; ++t) {
+          p.pos[t] = (uint32_t)bits[t].first;
+          p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
+        }
+        p.n_tuples = n_tuples;
+        CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
+      }
+    } else {
+      tanq::Gate3Params p;
+      int di = 0;
+      for (size_t i = 0; i < s->scratch.size(); ++i)
+        if (s->scratch[i].device == sh.device) di = (int)i;
+      p.Sfrag = (*frag3)[di];
+      for (int t = 0; t < 6; ++t) {
+        p.pos[t] = (uint32_t)bits[t].first;
+        p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
+      }
+      p.n_tuples = n_tuples;
+      CUDA_TRY(tanq::launch_gate3(sh.data, p, sh.stream));
+    }
+    s->launches++;
+    prof_end(s, sh, pr);
+  }
+  return TANQ_OK;
+}
+
+tanq_status ensure_frag_capacity(tanq_sim* s, DevScratch& d, size_t elems) {
+  if (d.frag_elems >= elems) return TANQ_OK;
+  CUDA_TRY(cudaSetDevice(d.device));
+  if (d.frag) CUDA_TRY(cudaFree(d.frag));
+  CUDA_TRY(cudaMalloc(&d.frag, elems * sizeof(double2)));
+  d.frag_elems = elems;
+  return TANQ_OK;
+}
+
+// Execute a list of fused ops in order (remaps inserted as needed).
+tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
+  // k=3 fragment staging: fragments depend on the layout at execution time, so they are
+  // built op by op into a pinned host ring and copied to each device before the launch.
+  size_t n3 = 0;
+  for (const auto& op : ops) n3 += op.k == 3;
+  const size_t fe = tanq::gate3_frag_elems();
+  double2* pinned = nullptr;
+  if (n3) {
+    for (auto& sh : s->shards) {
+      DevScratch& d = scratch_for(s, sh.device);
+      TRY(ensure_scratch(s, d));
+      TRY(ensure_frag_capacity(s, d, fe * n3));
+    }
+    CUDA_TRY(cudaMallocHost(&pinned, fe * n3 * sizeof(double2)));
+  }
+  size_t i3 = 0;
+  tanq_status st = TANQ_OK;
+  for (size_t i = 0; i < ops.size() && st == TANQ_OK; ++i) {
+    const FusedOp& op = ops[i];
+    st = ensure_local(s, op.k, op.q, &ops, i + 1);
+    if (st != TANQ_OK) break;
+    if (op.k == 3) {
+      std::vector<std::pair<int, int>> bits;
+      for (int j = 0; j < 3; ++j) {
+        bits.push_back({(int)s->phys[2 * op.q[j]], j});
+        bits.push_back({(int)s->phys[2 * op.q[j] + 1], 3 + j});
+      }
+      std::sort(bits.begin(), bits.end());
+      std::vector<double2> Sm(64 * 64);
+      int l_of[64];
+      for (int m = 0; m < 64; ++m) {
+        int l = 0;
+        for (int t = 0; t < 6; ++t)
+          if ((m >> t) & 1) l |= 1 << bits[t].second;
+        l_of[m] = l;
+      }
+      for (int a = 0; a < 64; ++a)
+        for (int b = 0; b < 64; ++b) {
+          cd v = op.S(l_of[a], l_of[b]);
+          Sm[a * 64 + b] = make_double2(v.real(), v.imag());
+        }
+      double2* hf = pinned + fe * i3;
+      tanq::gate3_make_frags(Sm.data(), hf);
+      std::vector<const double2*> ptrs(s->scratch.size(), nullptr);
+      for (auto& sh : s->shards) {
+        DevScratch& d = scratch_for(s, sh.device);
+        int di = 0;
+        for (size_t q = 0; q < s->scratch.size(); ++q)
+          if (s->scratch[q].device == sh.device) di = (int)q;
+        double2* dst = d.frag + fe * i3;
+        if (!ptrs[di]) {
+          CUDA_TRY(cudaSetDevice(sh.device));
+          CUDA_TRY(cudaMemcpyAsync(dst, hf, fe * sizeof(double2), cudaMemcpyHostToDevice,
+                                   sh.stream));
+          ptrs[di] = dst;
+        }
+      }
+      ++i3;
+      st = launch_op(s, op, &ptrs);
+    } else {
+      st = launch_op(s, op, nullptr);
+    }
+  }
+  if (pinned) {
+    tanq_status js = join_all(s);
+    cudaFreeHost(pinned);
+    if (st == TANQ_OK) st = js;
+  }
+  return st;
+}
+
+tanq_status check_qubits(const tanq_sim* s, int k, const int* q) {
+  if (k < 1 || k > 3) return fail(TANQ_E_ARG, "k must be 1..3");
+  if (!q) return fail(TANQ_E_ARG, "qubits is NULL");
+  for (int i = 0; i < k; ++i) {
+    if (q[i] < 0 || q[i] >= s->n) return fail(TANQ_E_ARG, "qubit out of range");
+    for (int j = 0; j < i; ++j)
+      if (q[i] == q[j]) return fail(TANQ_E_ARG, "repeated qubit");
+  }
+  if (2 * k > s->L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
+  return TANQ_OK;
+}
+
+Mat mat_from(const tanq_c64* m, int d) {
+  Mat M(d);
+  for (int i = 0; i < d * d; ++i) M.a[i] = cd(m[i].re, m[i].im);
+  return M;
+}
+
+bool finite_mat(const Mat& M) {
+  for (const cd& v : M.a)
+    if (!std::isfinite(v.real()) || !std::isfinite(v.imag())) return false;
+  return true;
+}
+
+// Noise binding (Sec. 3.5; readings R4-R10): one superoperator per circuit op.
+tanq_status bind_op(const tanq_sim* s, const tanq_op& op, const tanq_noise_model* nm,
+                    const std::map<std::tuple<int, int, int>, const tanq_gate_cal*>& cal,
+                    FusedOp& out) {
+  const int kind = op.kind;
+  if (kind < 0 || kind >= TANQ_N_KINDS) return fail(TANQ_E_ARG, "unknown op kind");
+  int k = kind_arity(kind);
+  if (k == 0) k = op.k;
+  if (kind_arity(kind) && op.k != 0 && op.k != k) return fail(TANQ_E_ARG, "k does not match gate");
+  TRY(check_qubits(s, k, op.q));
+  out.k = k;
+  for (int j = 0; j < k; ++j) out.q[j] = op.q[j];
+  const int d = 1 << k;
+  if (kind == TANQ_U || kind == TANQ_KRAUS || kind == TANQ_SUPEROP) {
+    if (!op.m) return fail(TANQ_E_ARG, "matrix payload is NULL");
+    if (kind == TANQ_U) {
+      Mat U = mat_from(op.m, d);
+      if (!finite_mat(U)) return fail(TANQ_E_ARG, "non-finite matrix");
+      out.S = superop_from_kraus({U});
+    } else if (kind == TANQ_KRAUS) {
+      if (op.n_kraus < 1) return fail(TANQ_E_ARG, "n_kraus < 1");
+      std::vector<Mat> Ks;
+      for (int i = 0; i < op.n_kraus; ++i) Ks.push_back(mat_from(op.m + (size_t)i * d * d, d));
+      out.S = superop_from_kraus(Ks);
+    } else {
+      out.S = mat_from(op.m, d * d);
+    }
+    if (!finite_mat(out.S)) return fail(TANQ_E_ARG, "non-finite matrix");
+    return TANQ_OK;
+  }
+  if ((kind == TANQ_RX || kind == TANQ_RY || kind == TANQ_RZ || kind == TANQ_CP) &&
+      !std::isfinite(op.theta))
+    return fail(TANQ_E_ARG, "non-finite theta");
+  Mat S = superop_from_kraus({gate_unitary(kind, op.theta)});
+  if (!nm || kind == TANQ_RZ) {  // RZ noiseless
+    out.S = S;
+    return TANQ_OK;
+  }
+  auto it = cal.find({kind, op.q[0], k == 2 ? op.q[1] : -1});
+  if (it == cal.end())
+    return fail(TANQ_E_ARG, "missing calibration for kind " + std::to_string(kind) + " on qubit " +
+                                std::to_string(op.q[0]));
+  const tanq_gate_cal& gc = *it->second;
+  if (gc.overrot_rad != 0.0) S = matmul(superop_from_kraus({overrot_unitary(k, gc.overrot_rad)}), S);
+  Mat Sth = identity(d * d);
+  bool has_th = false;
+  const double t_us = gc.duration_ns * 1e-3;
+  if (t_us > 0.0) {
+    for (int j = 0; j < k; ++j) {
+      const tanq_qubit_cal& qc = nm->qubits[op.q[j]];
+      if (qc.t1_us <= 0.0) continue;
+      Sth = matmul(embed_superop(superop_thermal(qc.t1_us, qc.t2_us, t_us), {j}, k), Sth);
+      has_th = true;
+    }
+  }
+  const bool has_dep = gc.depol_p != 0.0;
+  const Mat Sdep = has_dep ? superop_depol(k, gc.depol_p) : Mat();
+  if (nm->order == 0) {
+    if (has_th) S = matmul(Sth, S);
+    if (has_dep) S = matmul(Sdep, S);
+  } else {
+    if (has_dep) S = matmul(Sdep, S);
+    if (has_th) S = matmul(Sth, S);
+  }
+  out.S = S;
+  return TANQ_OK;
+}
+
+tanq_status validate_noise(const tanq_sim* s, const tanq_noise_model* nm,
+                           std::map<std::tuple<int, int, int>, const tanq_gate_cal*>& cal) {
+  if (!nm) return TANQ_OK;
+  if (nm->n != s->n || !nm->qubits) return fail(TANQ_E_ARG, "noise model size mismatch");
+  if (nm->order != 0 && nm->order != 1) return fail(TANQ_E_ARG, "noise order must be 0 or 1");
+  for (int q = 0; q < nm->n; ++q) {
+    const tanq_qubit_cal& qc = nm->qubits[q];
+    if (qc.t1_us > 0.0 && (!(qc.t2_us > 0.0) || qc.t2_us > 2.0 * qc.t1_us))
+      return fail(TANQ_E_ARG, "T2 must be in (0, 2 T1] on qubit " + std::to_string(q));
+  }
+  for (uint64_t i = 0; i < nm->n_gates; ++i) {
+    const tanq_gate_cal& g = nm->gates[i];
+    if (!(g.depol_p >= 0.0 && g.depol_p <= 1.0))
+      return fail(TANQ_E_ARG, "depolarizing p outside [0,1]");
+    if (!(g.duration_ns >= 0.0) || !std::isfinite(g.overrot_rad))
+      return fail(TANQ_E_ARG, "bad duration / over-rotation");
+    int k = kind_arity(g.kind);
+    if (k == 0) return fail(TANQ_E_ARG, "calibration for a non-named gate kind");
+    cal[{g.kind, g.q[0], k == 2 ? g.q[1] : -1}] = &g;
+  }
+  return TANQ_OK;
+}
+
+tanq_status apply_single(tanq_sim* s, FusedOp op) {
+  std::vector<FusedOp> ops{std::move(op)};
+  return exec_ops(s, ops);
+}
+
+tanq_status combine_probs(tanq_sim* s, DevScratch*& primary) {
+  // every shard writes its owned diagonal entries into its device's buffer
+  std::vector<DevScratch*> devs;
+  for (auto& sh : s->shards) {
+    DevScratch& d = scratch_for(s, sh.device);
+    TRY(ensure_scratch(s, d));
+    if (std::find(devs.begin(), devs.end(), &d) == devs.end()) {
+      devs.push_back(&d);
+      CUDA_TRY(cudaSetDevice(sh.device));
+      CUDA_TRY(cudaMemsetAsync(d.probs, 0, sizeof(double) << s->n, sh.stream));
+      CUDA_TRY(cudaMemsetAsync(d.imax, 0, sizeof(unsigned long long), sh.stream));
+    }
+  }
+  tanq::BitMap bm = bitmap_of(s);
+  for (auto& sh : s->shards) {
+    DevScratch& d = scratch_for(s, sh.device);
+    CUDA_TRY(cudaSetDevice(sh.device));
+    // shards sharing a device share a stream: order is implied; otherwise wait
+    CUDA_TRY(tanq::launch_diag(sh.data, d.probs, d.imax, bm, s->n, s->L, (uint64_t)sh.id,
+                               sh.stream));
+    s->launches++;
+  }
+  Shard& s0 = s->shards[0];
+  primary = &scratch_for(s, s0.device);
+  if (devs.size() > 1) {
+    for (auto& sh : s->shards) TRY(stream_wait(s0, sh));
+    CUDA_TRY(cudaSetDevice(s0.device));
+    for (DevScratch* d : devs) {
+      if (d == primary) continue;
+      CUDA_TRY(cudaMemcpyPeerAsync(primary->probs_tmp, s0.device, d->probs, d->device,
+                                   sizeof(double) << s->n, s0.stream));
+      CUDA_TRY(tanq::launch_add(primary->probs, primary->probs_tmp, (uint64_t)1 << s->n,
+                                s0.stream));
+      s->launches++;
+    }
+  }
+  if (s->dist && s->world > 1) {
+    CUDA_TRY(cudaSetDevice(s0.device));
+    NCCL_TRY(nccl().AllReduce(primary->probs, primary->probs, (size_t)1 << s->n, ncclDouble, ncclSum,
+                           s->comm, s0.stream));
+  }
+  // |Im diag| check
+  double imx = 0.0;
+  for (DevScratch* d : devs) {
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaSetDevice(d->device));
+    CUDA_TRY(cudaMemcpy(&bits, d->imax, sizeof(bits), cudaMemcpyDeviceToHost));
+    double v;
+    std::memcpy(&v, &bits, sizeof(v));
+    imx = std::max(imx, v);
+  }
+  if (imx >= 1e-6) return fail(TANQ_E_STATE, "|Im diag| = " + std::to_string(imx) + " >= 1e-6");
+  return TANQ_OK;
+}
+
+}  // namespace
+
+// ======================================================================================
+// C ABI
+// ======================================================================================
+static int ilog2(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+extern "C" {
+
+const char* tanq_last_error(void) { return g_err.c_str(); }
+
+static tanq_status create_common(int n, tanq_sim* s) {
+  const size_t shard_bytes = sizeof(double2) << s->L;
+  for (auto& sh : s->shards) {
+    CUDA_TRY(cudaSetDevice(sh.device));
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    int same = 0;
+    for (auto& o : s->shards) same += (o.device == sh.device && o.data == nullptr);
+    const size_t need = shard_bytes * (size_t)same + ((size_t)64 << 20) +
+                        (s->dist ? 2 * s->xchunk * sizeof(double2) : 0) + (sizeof(double) * 3 << n);
+    if (need > fr)
+      return fail(TANQ_E_NOMEM, "memory guard: need " + std::to_string(need) + " B, free " +
+                                    std::to_string(fr) + " B on device " +
+                                    std::to_string(sh.device));
+    // one stream per device (shards on the same device share it)
+    for (auto& o : s->shards)
+      if (o.device == sh.device && o.stream && &o != &sh) sh.stream = o.stream;
+    if (!sh.stream) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+      s->owned.push_back({sh.device, sh.stream});
+    }
+    CUDA_TRY(cudaMalloc(&sh.data, shard_bytes));
+    CUDA_TRY(tanq::launch_init(sh.data, (uint64_t)1 << s->L, sh.id == 0, sh.stream));
+    s->launches++;
+  }
+  // peer access between distinct devices
+  for (auto& a : s->shards)
+    for (auto& b : s->shards)
+      if (a.device != b.device) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, a.device, b.device);
+        if (ok) {
+          cudaSetDevice(a.device);
+          cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(TANQ_E_CUDA, "peer access");
+          cudaGetLastError();
+        }
+      }
+  reset_layout(s);
+  return TANQ_OK;
+}
+
+tanq_status tanq_create(int n_qubits, int n_shards, tanq_sim** out) {
+  if (!out) return fail(TANQ_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 24) return fail(TANQ_E_ARG, "n_qubits must be in [1, 24]");
+  if (n_shards != 1 && n_shards != 2 && n_shards != 4 && n_shards != 8)
+    return fail(TANQ_E_ARG, "n_shards must be 1, 2, 4 or 8");
+  const int L = 2 * n_qubits - ilog2(n_shards);
+  if (L < 2) return fail(TANQ_E_ARG, "too few local bits for this shard count");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(TANQ_E_UNSUPPORTED, "no CUDA device");
+  }
+  tanq_sim* s = new tanq_sim();
+  s->n = n_qubits;
+  s->L = L;
+  s->world = n_shards;
+  s->rank0 = 0;
+  for (int g = 0; g < n_shards; ++g) {
+    Shard sh;
+    sh.id = g;
+    sh.device = g % ndev;
+    s->shards.push_back(sh);
+  }
+  tanq_status st = create_common(n_qubits, s);
+  if (st != TANQ_OK) {
+    tanq_destroy(s);
+    return st;
+  }
+  *out = s;
+  return TANQ_OK;
+}
+
+tanq_status tanq_nccl_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId)) return fail(TANQ_E_ARG, "need 128 bytes");
+  ncclUniqueId id;
+  if (!nccl().ok) return fail(TANQ_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  NCCL_TRY(nccl().GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return TANQ_OK;
+}
+
+tanq_status tanq_create_dist(int n_qubits, int world_size, int rank, int device,
+                             const void* nccl_uid, tanq_sim** out) {
+  if (!out) return fail(TANQ_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 24) return fail(TANQ_E_ARG, "n_qubits must be in [1, 24]");
+  if (world_size != 1 && world_size != 2 && world_size != 4 && world_size != 8)
+    return fail(TANQ_E_ARG, "world_size must be 1, 2, 4 or 8");
+  if (rank < 0 || rank >= world_size) return fail(TANQ_E_ARG, "rank out of range");
+  if (world_size > 1 && !nccl_uid) return fail(TANQ_E_ARG, "nccl_uid required");
+  const int L = 2 * n_qubits - ilog2(world_size);
+  if (L < 2) return fail(TANQ_E_ARG, "too few local bits for this world size");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(TANQ_E_UNSUPPORTED, "no CUDA device");
+  }
+  if (device < 0 || device >= ndev) return fail(TANQ_E_ARG, "device out of range");
+  tanq_sim* s = new tanq_sim();
+  s->n = n_qubits;
+  s->L = L;
+  s->world = world_size;
+  s->rank0 = rank;
+  s->dist = true;
+  Shard sh;
+  sh.id = rank;
+  sh.device = device;
+  s->shards.push_back(sh);
+  s->xchunk = std::min<size_t>((size_t)1 << 24, (size_t)1 << (L > 1 ? L - 1 : 0));  // 256 MiB
+  tanq_status st = create_common(n_qubits, s);
+  if (st == TANQ_OK && world_size > 1) {
+    cudaSetDevice(device);
+    if (cudaMalloc(&s->xsend, s->xchunk * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&s->xrecv, s->xchunk * sizeof(double2)) != cudaSuccess)
+      st = fail(TANQ_E_NOMEM, "staging");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_uid, sizeof(id));
+    if (st == TANQ_OK) {
+      if (!nccl().ok) {
+        st = fail(TANQ_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+      } else {
+        ncclResult_t r = nccl().CommInitRank(&s->comm, world_size, id, rank);
+        if (r != ncclSuccess) st = fail(TANQ_E_NCCL, nccl().GetErrorString(r));
+      }
+    }
+  }
+  if (st != TANQ_OK) {
+    tanq_destroy(s);
+    return st;
+  }
+  *out = s;
+  return TANQ_OK;
+}
+
+tanq_status tanq_destroy(tanq_sim* s) {
+  if (!s) return TANQ_OK;
+  for (auto& p : s->prof) {
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  for (auto& sh : s->shards) {
+    cudaSetDevice(sh.device);
+    if (sh.stream) cudaStreamSynchronize(sh.stream);
+    if (sh.data) cudaFree(sh.data);
+  }
+  for (auto& p : s->owned) {
+    cudaSetDevice(p.first);
+    cudaStreamDestroy(p.second);
+  }
+  for (auto& d : s->scratch) {
+    cudaSetDevice(d.device);
+    cudaFree(d.probs);
+    cudaFree(d.probs_tmp);
+    cudaFree(d.cdf);
+    cudaFree(d.partial);
+    cudaFree(d.scal);
+    cudaFree(d.imax);
+    cudaFree(d.stage);
+    cudaFree(d.frag);
+  }
+  if (s->xsend) cudaFree(s->xsend);
+  if (s->xrecv) cudaFree(s->xrecv);
+  if (s->comm) nccl().CommDestroy(s->comm);
+  cudaGetLastError();
+  delete s;
+  return TANQ_OK;
+}
+
+tanq_status tanq_reset(tanq_sim* s) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  for (auto& sh : s->shards) {
+    CUDA_TRY(cudaSetDevice(sh.device));
+    CUDA_TRY(tanq::launch_init(sh.data, (uint64_t)1 << s->L, sh.id == 0, sh.stream));
+    s->launches++;
+  }
+  reset_layout(s);
+  return TANQ_OK;
+}
+
+tanq_status tanq_info_get(tanq_sim* s, tanq_info* o) {
+  if (!s || !o) return fail(TANQ_E_ARG, "NULL");
+  std::memset(o, 0, sizeof(*o));
+  o->n_qubits = s->n;
+  o->n_shards = (int)s->shards.size();
+  o->world_size = s->world;
+  o->rank = s->rank0;
+  o->local_bits = s->L;
+  for (int q = 0; q < s->n && q < 32; ++q) {
+    o->rowpos[q] = (int)s->phys[2 * q];
+    o->colpos[q] = (int)s->phys[2 * q + 1];
+  }
+  o->shard_bytes = sizeof(double2) << s->L;
+  return TANQ_OK;
+}
+
+tanq_status tanq_set_stream(tanq_sim* s, int shard, void* stream) {
+  if (!s || shard < 0 || shard >= (int)s->shards.size()) return fail(TANQ_E_ARG, "bad shard");
+  Shard& sh = s->shards[shard];
+  CUDA_TRY(cudaSetDevice(sh.device));
+  CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  cudaStream_t ns = stream ? (cudaStream_t)stream : s->own_streams_of(sh.device);
+  for (auto& o : s->shards)
+    if (o.device == sh.device) o.stream = ns;
+  return TANQ_OK;
+}
+
+tanq_status tanq_apply_gate(tanq_sim* s, int k, const int* qubits, const tanq_c64* U) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  TRY(check_qubits(s, k, qubits));
+  if (!U) return fail(TANQ_E_ARG, "U is NULL");
+  FusedOp op;
+  op.k = k;
+  for (int j = 0; j < k; ++j) op.q[j] = qubits[j];
+  Mat G = mat_from(U, 1 << k);
+  if (!finite_mat(G)) return fail(TANQ_E_ARG, "non-finite matrix");
+  op.S = superop_from_kraus({G});
+  return apply_single(s, std::move(op));
+}
+
+tanq_status tanq_apply_channel(tanq_sim* s, int k, const int* qubits, int m, const tanq_c64* kraus,
+                               int check_cptp) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  TRY(check_qubits(s, k, qubits));
+  if (!kraus || m < 1) return fail(TANQ_E_ARG, "empty Kraus list");
+  const int d = 1 << k;
+  std::vector<Mat> Ks;
+  for (int i = 0; i < m; ++i) {
+    Ks.push_back(mat_from(kraus + (size_t)i * d * d, d));
+    if (!finite_mat(Ks.back())) return fail(TANQ_E_ARG, "non-finite matrix");
+  }
+  if (check_cptp) {
+    Mat sum(d);
+    for (const Mat& K : Ks)
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+          for (int l = 0; l < d; ++l) sum(i, j) += std::conj(K(l, i)) * K(l, j);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j)
+        if (std::abs(sum(i, j) - (i == j ? 1.0 : 0.0)) > 1e-12)
+          return fail(TANQ_E_ARG, "channel is not trace preserving (sum K^dag K != I)");
+  }
+  FusedOp op;
+  op.k = k;
+  for (int j = 0; j < k; ++j) op.q[j] = qubits[j];
+  op.S = superop_from_kraus(Ks);
+  return apply_single(s, std::move(op));
+}
+
+tanq_status tanq_apply_superop(tanq_sim* s, int k, const int* qubits, const tanq_c64* S) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  TRY(check_qubits(s, k, qubits));
+  if (!S) return fail(TANQ_E_ARG, "S is NULL");
+  FusedOp op;
+  op.k = k;
+  for (int j = 0; j < k; ++j) op.q[j] = qubits[j];
+  op.S = mat_from(S, 1 << (2 * k));
+  if (!finite_mat(op.S)) return fail(TANQ_E_ARG, "non-finite matrix");
+  return apply_single(s, std::move(op));
+}
+
+}  // extern "C"
+
+struct tanq_plan {
+  int n = 0;
+  std::vector<FusedOp> ops;
+  uint64_t ops_in = 0;
+  double plan_ms = 0;
+  int flags = 0;
+};
+
+extern "C" {
+
+static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_noise_model* nm,
+                               const tanq_run_opts* o, tanq_plan** out) {
+  if (!c || !out) return fail(TANQ_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (c->n_ops && !c->ops) return fail(TANQ_E_ARG, "ops is NULL");
+  tanq_run_opts opts{2, 2, 0, 0, 0};
+  if (o) opts = *o;
+  if (opts.fuse < 0 || opts.fuse > 2) return fail(TANQ_E_ARG, "fuse must be 0, 1 or 2");
+  if (opts.k_max < 1 || opts.k_max > 3) return fail(TANQ_E_ARG, "k_max must be 1..3");
+  if (opts.k_max == 3 && L < 6) opts.k_max = 2;
+  const auto t0 = std::chrono::steady_clock::now();
+  tanq_sim shape;  // only n and L are read by the validators
+  shape.n = n;
+  shape.L = L;
+  std::map<std::tuple<int, int, int>, const tanq_gate_cal*> cal;
+  TRY(validate_noise(&shape, nm, cal));
+  std::vector<FusedOp> ops;
+  ops.reserve(c->n_ops);
+  for (uint64_t i = 0; i < c->n_ops; ++i) {
+    FusedOp f;
+    TRY(bind_op(&shape, c->ops[i], nm, cal, f));
+    ops.push_back(std::move(f));
+  }
+  tanq_plan* p = new tanq_plan();
+  p->n = n;
+  p->ops = fuse(ops, opts.fuse, opts.k_max);
+  p->ops_in = c->n_ops;
+  p->flags = opts.flags;
+  p->plan_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = p;
+  return TANQ_OK;
+}
+
+tanq_status tanq_plan_create(tanq_sim* s, const tanq_circuit* c, const tanq_noise_model* nm,
+                             const tanq_run_opts* o, tanq_plan** out) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  return plan_create(s->n, s->L, c, nm, o, out);
+}
+
+tanq_status tanq_plan_create_host(int n_qubits, int world_size, const tanq_circuit* c,
+                                  const tanq_noise_model* nm, const tanq_run_opts* o,
+                                  tanq_plan** out) {
+  if (n_qubits < 1 || n_qubits > 24) return fail(TANQ_E_ARG, "n_qubits must be in [1, 24]");
+  if (world_size != 1 && world_size != 2 && world_size != 4 && world_size != 8)
+    return fail(TANQ_E_ARG, "world_size must be 1, 2, 4 or 8");
+  const int L = 2 * n_qubits - ilog2(world_size);
+  if (L < 2) return fail(TANQ_E_ARG, "too few local bits");
+  return plan_create(n_qubits, L, c, nm, o, out);
+}
+
+tanq_status tanq_plan_info(const tanq_plan* p, tanq_run_stats* st) {
+  if (!p || !st) return fail(TANQ_E_ARG, "NULL argument");
+  std::memset(st, 0, sizeof(*st));
+  st->ops_in = p->ops_in;
+  st->ops_fused = p->ops.size();
+  for (const auto& f : p->ops) st->n_k[f.k]++;
+  st->plan_ms = p->plan_ms;
+  return TANQ_OK;
+}
+
+tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits, tanq_c64* S) {
+  if (!p || !k || !qubits) return fail(TANQ_E_ARG, "NULL argument");
+  if (i >= p->ops.size()) return fail(TANQ_E_ARG, "op index out of range");
+  const FusedOp& f = p->ops[i];
+  *k = f.k;
+  for (int j = 0; j < f.k; ++j) qubits[j] = f.q[j];
+  if (S)
+    for (size_t e = 0; e < f.S.a.size(); ++e) S[e] = tanq_c64{f.S.a[e].real(), f.S.a[e].imag()};
+  return TANQ_OK;
+}
+
+tanq_status tanq_plan_exec(tanq_sim* s, const tanq_plan* p, tanq_run_stats* st) {
+  if (!s || !p) return fail(TANQ_E_ARG, "NULL argument");
+  if (p->n != s->n) return fail(TANQ_E_ARG, "plan built for a different register size");
+  for (const auto& f : p->ops)
+    if (2 * f.k > s->L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
+  const uint64_t r0 = s->remap_count, b0 = s->remap_bytes;
+  s->prof_on = (p->flags & 1) != 0;
+  tanq_status r = exec_ops(s, p->ops);
+  s->prof_on = false;
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->ops_in = p->ops_in;
+    st->ops_fused = p->ops.size();
+    for (const auto& f : p->ops) st->n_k[f.k]++;
+    st->n_remaps = s->remap_count - r0;
+    st->remap_bytes = s->remap_bytes - b0;
+    st->plan_ms = p->plan_ms;
+  }
+  return r;
+}
+
+tanq_status tanq_plan_destroy(tanq_plan* p) {
+  delete p;
+  return TANQ_OK;
+}
+
+tanq_status tanq_run_circuit(tanq_sim* s, const tanq_circuit* c, const tanq_noise_model* nm,
+                             const tanq_run_opts* o, tanq_run_stats* st) {
+  tanq_plan* p = nullptr;
+  TRY(tanq_plan_create(s, c, nm, o, &p));
+  tanq_status r = tanq_plan_exec(s, p, st);
+  tanq_plan_destroy(p);
+  return r;
+}
+
+tanq_status tanq_probs(tanq_sim* s, const tanq_readout* ro, double* probs) {
+  if (!s || !probs) return fail(TANQ_E_ARG, "NULL argument");
+  if (ro) {
+    for (int q = 0; q < s->n; ++q) {
+      double a = ro->p10 ? ro->p10[q] : 0.0, b = ro->p01 ? ro->p01[q] : 0.0;
+      if (!(a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0))
+        return fail(TANQ_E_ARG, "readout probability outside [0,1]");
+    }
+  }
+  DevScratch* pd = nullptr;
+  TRY(combine_probs(s, pd));
+  Shard& s0 = s->shards[0];
+  CUDA_TRY(cudaSetDevice(s0.device));
+  if (ro) {
+    CUDA_TRY(tanq::launch_readout(pd->probs, s->n, ro->p10, ro->p01, s0.stream));
+    s->launches += s->n;
+  }
+  CUDA_TRY(cudaMemcpyAsync(probs, pd->probs, sizeof(double) << s->n, cudaMemcpyDeviceToHost,
+                           s0.stream));
+  CUDA_TRY(cudaStreamSynchronize(s0.stream));
+  return TANQ_OK;
+}
+
+tanq_status tanq_expect_pauli(tanq_sim* s, uint64_t xm, uint64_t zm, double* out_re,
+                              double* out_im) {
+  if (!s || !out_re) return fail(TANQ_E_ARG, "NULL argument");
+  const uint64_t lim = s->n >= 64 ? ~0ull : ((1ull << s->n) - 1);
+  if ((xm & ~lim) || (zm & ~lim)) return fail(TANQ_E_ARG, "Pauli mask outside the register");
+  tanq::BitMap bm = bitmap_of(s);
+  const int nb = tanq::expect_blocks(s->n);
+  double re = 0.0, im = 0.0;
+  std::vector<double2> host(s->shards.size());
+  for (size_t i = 0; i < s->shards.size(); ++i) {
+    Shard& sh = s->shards[i];
+    DevScratch& d = scratch_for(s, sh.device);
+    TRY(ensure_scratch(s, d));
+    CUDA_TRY(cudaSetDevice(sh.device));
+    CUDA_TRY(tanq::launch_expect(sh.data, d.partial, nb, bm, s->n, s->L, (uint64_t)sh.id, xm, zm,
+                                 sh.stream));
+    CUDA_TRY(tanq::launch_reduce_partials(d.partial, nb, d.scal, sh.stream));
+    s->launches += 2;
+    if (s->dist && s->world > 1)
+      NCCL_TRY(nccl().AllReduce(d.scal, d.scal, 2, ncclDouble, ncclSum, s->comm, sh.stream));
+    CUDA_TRY(cudaMemcpyAsync(&host[i], d.scal, sizeof(double2), cudaMemcpyDeviceToHost,
+                             sh.stream));
+    CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  }
+  for (auto& v : host) {
+    re += v.x;
+    im += v.y;
+  }
+  // global factor (-i)^{popc(x & z)}
+  switch (__builtin_popcountll(xm & zm) & 3) {
+    case 0: break;
+    case 1: { double t = re; re = im; im = -t; break; }
+    case 2: re = -re; im = -im; break;
+    case 3: { double t = re; re = -im; im = t; break; }
+  }
+  *out_re = re;
+  if (out_im) *out_im = im;
+  return TANQ_OK;
+}
+
+tanq_status tanq_sample(tanq_sim* s, const tanq_readout* ro, uint64_t seed, uint64_t shots,
+                        uint64_t* outcomes) {
+  if (!s || (!outcomes && shots)) return fail(TANQ_E_ARG, "NULL argument");
+  if (shots == 0) return TANQ_OK;
+  DevScratch* pd = nullptr;
+  TRY(combine_probs(s, pd));
+  Shard& s0 = s->shards[0];
+  CUDA_TRY(cudaSetDevice(s0.device));
+  if (ro) {
+    CUDA_TRY(tanq::launch_readout(pd->probs, s->n, ro->p10, ro->p01, s0.stream));
+    s->launches += s->n;
+  }
+  CUDA_TRY(tanq::launch_cdf(pd->probs, pd->cdf, s->n, s0.stream));
+  unsigned long long* dout = nullptr;
+  CUDA_TRY(cudaMallocAsync(&dout, shots * sizeof(unsigned long long), s0.stream));
+  CUDA_TRY(tanq::launch_sample(pd->cdf, s->n, seed, shots, dout, s0.stream));
+  s->launches += 2;
+  CUDA_TRY(cudaMemcpyAsync(outcomes, dout, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           s0.stream));
+  CUDA_TRY(cudaFreeAsync(dout, s0.stream));
+  CUDA_TRY(cudaStreamSynchronize(s0.stream));
+  return TANQ_OK;
+}
+
+static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c64* out,
+                            const tanq_c64* in) {
+  const uint64_t total = (uint64_t)1 << (2 * s->n);
+  if (first > total || count > total - first) return fail(TANQ_E_ARG, "range outside vec(rho)");
+  if (!count) return TANQ_OK;
+  tanq::BitMap bm = bitmap_of(s);
+  bool multi_dev = false;
+  for (auto& sh : s->shards) multi_dev |= sh.device != s->shards[0].device;
+  std::vector<double2> acc;
+  for (auto& sh : s->shards) {
+    DevScratch& d = scratch_for(s, sh.device);
+    TRY(ensure_scratch(s, d));
+  }
+  const size_t chunk = scratch_for(s, s->shards[0].device).stage_elems;
+  for (uint64_t off = 0; off < count; off += chunk) {
+    const uint64_t cnt = std::min<uint64_t>(chunk, count - off);
+    if (in) {
+      for (auto& sh : s->shards) {
+        DevScratch& d = scratch_for(s, sh.device);
+        CUDA_TRY(cudaSetDevice(sh.device));
+        CUDA_TRY(cudaMemcpyAsync(d.stage, in + off, cnt * sizeof(double2), cudaMemcpyHostToDevice,
+                                 sh.stream));
+        CUDA_TRY(tanq::launch_scatter_vec(sh.data, d.stage, bm, s->n, s->L, (uint64_t)sh.id,
+                                          first + off, cnt, sh.stream));
+        s->launches++;
+        CUDA_TRY(cudaStreamSynchronize(sh.stream));
+      }
+      continue;
+    }
+    const bool need_sum = multi_dev || (s->dist && s->world > 1);
+    if (need_sum) {
+      acc.assign(cnt, make_double2(0.0, 0.0));
+      std::vector<double2> tmp(cnt);
+      for (auto& sh : s->shards) {
+        DevScratch& d = scratch_for(s, sh.device);
+        CUDA_TRY(cudaSetDevice(sh.device));
+        CUDA_TRY(tanq::launch_gather_vec(sh.data, d.stage, bm, s->n, s->L, (uint64_t)sh.id,
+                                         first + off, cnt, true, sh.stream));
+        s->launches++;
+        if (s->dist)
+          NCCL_TRY(nccl().AllReduce(d.stage, d.stage, cnt * 2, ncclDouble, ncclSum, s->comm,
+                                 sh.stream));
+        CUDA_TRY(cudaMemcpyAsync(tmp.data(), d.stage, cnt * sizeof(double2),
+                                 cudaMemcpyDeviceToHost, sh.stream));
+        CUDA_TRY(cudaStreamSynchronize(sh.stream));
+        for (uint64_t i = 0; i < cnt; ++i) {  // exactly one shard owns each entry: x + 0
+          acc[i].x += tmp[i].x;
+          acc[i].y += tmp[i].y;
+        }
+      }
+      std::memcpy(out + off, acc.data(), cnt * sizeof(double2));
+    } else {
+      Shard& s0 = s->shards[0];
+      DevScratch& d = scratch_for(s, s0.device);
+      CUDA_TRY(cudaSetDevice(s0.device));
+      for (auto& sh : s->shards) {
+        CUDA_TRY(tanq::launch_gather_vec(sh.data, d.stage, bm, s->n, s->L, (uint64_t)sh.id,
+                                         first + off, cnt, false, sh.stream));
+        s->launches++;
+      }
+      CUDA_TRY(cudaMemcpyAsync(out + off, d.stage, cnt * sizeof(double2), cudaMemcpyDeviceToHost,
+                               s0.stream));
+      CUDA_TRY(cudaStreamSynchronize(s0.stream));
+    }
+  }
+  return TANQ_OK;
+}
+
+tanq_status tanq_get_state(tanq_sim* s, uint64_t first, uint64_t count, tanq_c64* out) {
+  if (!s || (!out && count)) return fail(TANQ_E_ARG, "NULL argument");
+  return state_io(s, first, count, out, nullptr);
+}
+
+tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const tanq_c64* in) {
+  if (!s || (!in && count)) return fail(TANQ_E_ARG, "NULL argument");
+  return state_io(s, first, count, nullptr, in);
+}
+
+tanq_status tanq_sync(tanq_sim* s) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  TRY(join_all(s));
+  CUDA_TRY(cudaGetLastError());
+  return TANQ_OK;
+}
+
+tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* n_out) {
+  if (!s || !n_out) return fail(TANQ_E_ARG, "NULL argument");
+  TRY(prof_flush(s));
+  int n = 0;
+  for (int c = 0; c < 4 && n < max; ++c) {
+    if (!s->prof_launches[c]) continue;
+    tanq_kernel_prof& p = out[n++];
+    std::memset(&p, 0, sizeof(p));
+    std::strncpy(p.name, kProfNames[c], sizeof(p.name) - 1);
+    p.launches = s->prof_launches[c];
+    p.total_ms = s->prof_ms[c];
+    p.bytes = s->prof_bytes[c];
+    p.flops = s->prof_flops[c];
+  }
+  *n_out = n;
+  return TANQ_OK;
+}
+
+tanq_status tanq_profile_reset(tanq_sim* s) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  TRY(prof_flush(s));
+  for (int c = 0; c < 4; ++c) {
+    s->prof_ms[c] = s->prof_bytes[c] = s->prof_flops[c] = 0;
+    s->prof_launches[c] = 0;
+  }
+  return TANQ_OK;
+}
+
+uint64_t tanq_launch_count(tanq_sim* s) { return s ? s->launches : 0; }
+
+}  // extern "C"

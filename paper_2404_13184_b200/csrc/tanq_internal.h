@@ -1,0 +1,84 @@
+// Internal interface between the host planner (tanq_host.cpp) and the sm_100a kernels
+// (tanq_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tanq {
+
+// A gate launch: apply a dense 4^K x 4^K complex matrix to every tuple of one shard.
+// Member i of a tuple sits at physical offset base + sum_j bit_j(i) << pos[j], where
+// pos[0] < pos[1] < ... < pos[2K-1] are the op's physical target bits (all local);
+// base is the tuple index with zero bits inserted at pos[] (Eq. 4's s_i generalised,
+// P:82-98).  S is stored in member order (the host permutes the paper's r + c 2^k order).
+template <int K>
+struct GateParams {
+  static constexpr int M = 1 << (2 * K);
+  double2 S[M * M];
+  uint64_t lo_mask[2 * K];   // (1 << pos[j]) - 1
+  uint64_t n_tuples;         // 2^(L - 2K)
+  uint32_t pos[2 * K];
+};
+
+// K = 3: the superoperator is 64 x 64 complex = 64 KiB, too large for a kernel parameter;
+// it lives in global memory pre-arranged in DMMA fragment order (see tanq_kernels.cu).
+struct Gate3Params {
+  const double2* Sfrag;      // [8 m-tiles][16 k-steps][32 lanes] of (Sr, Si)
+  uint64_t lo_mask[6];
+  uint64_t n_tuples;
+  uint32_t pos[6];
+};
+
+struct BitMap {               // physical bit of each logical bit (row q -> 2q, col q -> 2q+1)
+  uint32_t phys[64];
+  int nbits;                 // 2n
+};
+
+// kernel launchers (all asynchronous on `st`)
+cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st);
+cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st);
+cudaError_t launch_gate3(double2* a, const Gate3Params& p, cudaStream_t st);
+size_t gate3_frag_elems();   // double2 count of the fragment-ordered S
+void gate3_make_frags(const double2* S_member_order /*64x64*/, double2* frag /*host*/);
+
+cudaError_t launch_init(double2* a, uint64_t elems, bool one_at_zero, cudaStream_t st);
+// In-place swap of the halves two shards exchange when global bit g swaps with local bit b:
+// element e in [0, 2^(L-1)): j = e >> b, low = e & (2^b - 1);
+//   A[(j << (b+1)) | (va << b) | low]  <->  B[(j << (b+1)) | (vb << b) | low]
+cudaError_t launch_swap_halves(double2* A, double2* B, int L, int b, int va, int vb,
+                               cudaStream_t st);
+// pack / unpack the half {o : bit_b(o) == v} of a shard to / from a contiguous buffer,
+// elements [first, first + count) of the half in run order.
+cudaError_t launch_pack_half(const double2* a, double2* buf, int b, int v, uint64_t first,
+                             uint64_t count, cudaStream_t st);
+cudaError_t launch_unpack_half(double2* a, const double2* buf, int b, int v, uint64_t first,
+                               uint64_t count, cudaStream_t st);
+
+// Paper vec index v = r + c 2^n  <->  physical index; gather / scatter the owned entries
+// of a range [first, first+count) of vec(rho) for shard `shard` (local bits L).
+cudaError_t launch_gather_vec(const double2* a, double2* out, const BitMap& bm, int n, int L,
+                              uint64_t shard, uint64_t first, uint64_t count, bool zero_unowned,
+                              cudaStream_t st);
+cudaError_t launch_scatter_vec(double2* a, const double2* in, const BitMap& bm, int n, int L,
+                               uint64_t shard, uint64_t first, uint64_t count, cudaStream_t st);
+
+// probs[x] = Re rho[x][x] for owned x (others untouched); atomically max |Im| into *imax
+// (as the bit pattern of a non-negative double).
+cudaError_t launch_diag(const double2* a, double* probs, unsigned long long* imax,
+                        const BitMap& bm, int n, int L, uint64_t shard, cudaStream_t st);
+cudaError_t launch_readout(double* p, int n, const double* p10, const double* p01,
+                           cudaStream_t st);
+// Partial sums of (-1)^{popc(a & z)} rho[a ^ x][a] over owned a into partial[blocks] (re, im)
+cudaError_t launch_expect(const double2* a, double2* partial, int nblocks, const BitMap& bm,
+                          int n, int L, uint64_t shard, uint64_t xm, uint64_t zm,
+                          cudaStream_t st);
+int expect_blocks(int n);
+cudaError_t launch_reduce_partials(const double2* partial, int nblocks, double2* out,
+                                   cudaStream_t st);
+// sampling: clamp + inclusive scan (single CTA), then Philox draws + binary search
+cudaError_t launch_cdf(const double* p, double* cdf, int n, cudaStream_t st);
+cudaError_t launch_sample(const double* cdf, int n, uint64_t seed, uint64_t shots,
+                          unsigned long long* out, cudaStream_t st);
+cudaError_t launch_add(double* dst, const double* src, uint64_t count, cudaStream_t st);
+
+}  // namespace tanq

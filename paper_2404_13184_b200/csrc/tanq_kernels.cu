@@ -1,0 +1,625 @@
+// sm_100a kernels of the TANQ hot path.
+//
+//   K1/K2  gate_kernel<K>   FMA register stream: 4^K-member tuple gathered with 16 B (or,
+//                           when physical bit 0 is a target bit, 32 B) loads, y = S x with S
+//                           read from the kernel-parameter constant bank, written in place.
+//   K3     gate3_kernel     fused 3-qubit ops: 64x64 complex superoperator on the FP64
+//                           tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4), tuples staged
+//                           through shared memory with cp.async, 3-real-multiply complex GEMM.
+//   remap  swap/pack/unpack, vec<->physical gather/scatter, diagonal, readout, Pauli
+//          expectation, CDF + Philox sampling.
+//
+// Paper: each op performs 4^{n-k} independent [4^k x 4^k] x [4^k] complex mat-vecs on the
+// tuples of Eq. 4; the tuple base s_i is the tuple index with zero bits inserted
+// at the target positions (generalised to arbitrary physical bit positions here).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "tanq_internal.h"
+
+namespace tanq {
+
+static constexpr int kThreads = 256;
+
+static inline unsigned grid_for(uint64_t work, int threads, uint64_t cap = 148ull * 64) {
+  uint64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+__device__ __forceinline__ uint64_t insert_zeros(uint64_t t, const uint64_t* lo, int cnt) {
+#pragma unroll
+  for (int j = 0; j < 6; ++j)
+    if (j < cnt) t = ((t & ~lo[j]) << 1) | (t & lo[j]);
+  return t;
+}
+
+__device__ __forceinline__ void ld32(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+__device__ __forceinline__ void st32(double2* p, const double2& a, const double2& b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x),
+               "d"(b.y)
+               : "memory");
+}
+
+// ------------------------------------------------------------------------------------
+// K1 / K2: FMA register stream
+// ------------------------------------------------------------------------------------
+template <int K, bool PAIR>
+__global__ void __launch_bounds__(kThreads)
+    gate_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<K> p) {
+  constexpr int M = 1 << (2 * K);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.n_tuples; t += stride) {
+    uint64_t base = t;
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) base = ((base & ~p.lo_mask[j]) << 1) | (base & p.lo_mask[j]);
+    double2* ptr = a + base;
+    uint64_t off[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      uint64_t o = 0;
+#pragma unroll
+      for (int j = 0; j < 2 * K; ++j)
+        if ((i >> j) & 1) o += (uint64_t)1 << p.pos[j];
+      off[i] = o;
+    }
+    double2 x[M];
+    if constexpr (PAIR) {
+#pragma unroll
+      for (int i = 0; i < M; i += 2) ld32(ptr + off[i], x[i], x[i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < M; ++i) x[i] = ptr[off[i]];
+    }
+#pragma unroll
+    for (int l = 0; l < M; l += 2) {
+      double2 y[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double yr = 0.0, yi = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const double2 s = p.S[(l + u) * M + m];
+          yr = fma(s.x, x[m].x, yr);
+          yr = fma(-s.y, x[m].y, yr);
+          yi = fma(s.x, x[m].y, yi);
+          yi = fma(s.y, x[m].x, yi);
+        }
+        y[u] = make_double2(yr, yi);
+      }
+      if constexpr (PAIR) {
+        st32(ptr + off[l], y[0], y[1]);
+      } else {
+        ptr[off[l]] = y[0];
+        ptr[off[l + 1]] = y[1];
+      }
+    }
+  }
+}
+
+template <int K>
+static cudaError_t launch_gate_impl(double2* a, const GateParams<K>& p, cudaStream_t st) {
+  // grid-stride: up to 32 resident 256-thread waves per SM-count multiple
+  unsigned grid = grid_for(p.n_tuples, kThreads, 148ull * 256);
+  if (p.pos[0] == 0)
+    gate_kernel<K, true><<<grid, kThreads, 0, st>>>(a, p);
+  else
+    gate_kernel<K, false><<<grid, kThreads, 0, st>>>(a, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st) {
+  return launch_gate_impl<1>(a, p, st);
+}
+cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
+  return launch_gate_impl<2>(a, p, st);
+}
+
+// ------------------------------------------------------------------------------------
+// K3: fused 3-qubit superoperator on DMMA.8x8x4 (mma.sync.m8n8k4 f64)
+//
+// Per warp: a tile of 8 tuples.  Complex Y[64 x 8] = S[64 x 64] X[64 x 8] with the
+// 3-multiply form  P1 = Sr Xr, P2 = Si Xi, P3 = (Sr + Si)(Xr + Xi);
+// Yr = P1 - P2, Yi = P3 - P1 - P2.
+// Fragments (PTX m8n8k4 .row.col f64): A[8x4] lane -> (lane>>2, lane&3);
+// B[4x8] lane -> (k = lane&3, n = lane>>2); D[8x8] lane -> (lane>>2, 2*(lane&3)+{0,1}).
+// A = S rows 8mt.., cols 4ks..; the host stores S as frag[mt][ks][lane] = (Sr, Si, Sr+Si).
+// X tiles: shared [64 members][8 tuples] double2, double-buffered per warp, cp.async.
+// ------------------------------------------------------------------------------------
+static constexpr int k3Warps = 8;
+static constexpr int k3FragElems = 8 * 16 * 32;  // (Sr, Si) per (m-tile, k-step, lane)
+
+size_t gate3_frag_elems() { return (size_t)k3FragElems; }
+
+void gate3_make_frags(const double2* S, double2* frag) {
+  // frag[(mt*16 + ks)*32 + lane] = S[8 mt + (lane>>2)][4 ks + (lane&3)]  (A fragment order)
+  for (int mt = 0; mt < 8; ++mt)
+    for (int ks = 0; ks < 16; ++ks)
+      for (int lane = 0; lane < 32; ++lane) {
+        int row = mt * 8 + (lane >> 2), col = ks * 4 + (lane & 3);
+        frag[((size_t)mt * 16 + ks) * 32 + lane] = S[row * 64 + col];
+      }
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__global__ void __launch_bounds__(k3Warps * 32, 1)
+    gate3_kernel(double2* __restrict__ a, const __grid_constant__ Gate3Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // shared: S fragments (Sr, Si) 64 KiB | X tiles 8 warps x 2 buffers x 512 double2 128 KiB |
+  //         member offsets 64 x 8 B.  Sr + Si is formed in registers.
+  double2* sS = reinterpret_cast<double2*>(smem_raw);
+  double2* sX = sS + k3FragElems;
+  uint64_t* sOff = reinterpret_cast<uint64_t*>(sX + k3Warps * 2 * 512);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int e = threadIdx.x; e < k3FragElems; e += blockDim.x) sS[e] = p.Sfrag[e];
+  for (int m = threadIdx.x; m < 64; m += blockDim.x) {
+    uint64_t o = 0;
+    for (int j = 0; j < 6; ++j)
+      if ((m >> j) & 1) o += (uint64_t)1 << p.pos[j];
+    sOff[m] = o;
+  }
+  __syncthreads();
+
+  const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
+  const uint64_t tile_stride = (uint64_t)gridDim.x * k3Warps;
+  uint64_t tile = (uint64_t)blockIdx.x * k3Warps + warp;
+  double2* bufs[2] = {sX + warp * 2 * 512, sX + warp * 2 * 512 + 512};
+  const int ld_t = lane & 7, ld_m0 = lane >> 3;  // load/store mapping: tuple, member base
+
+  auto issue_load = [&](uint64_t tl, double2* buf) {
+    uint64_t t = tl * 8 + ld_t;
+    bool ok = t < p.n_tuples;
+    uint64_t base = insert_zeros(ok ? t : 0, p.lo_mask, 6);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      int m = ld_m0 + 4 * i;
+      cp_async16(buf + m * 8 + ld_t, a + base + sOff[m], ok);
+    }
+    cp_async_commit();
+  };
+
+  if (tile < n_tiles) issue_load(tile, bufs[0]);
+  int cur = 0;
+  for (; tile < n_tiles; tile += tile_stride) {
+    const uint64_t next = tile + tile_stride;
+    if (next < n_tiles) {
+      issue_load(next, bufs[cur ^ 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    double2* X = bufs[cur];
+    double p1[8][2], p2[8][2], p3[8][2];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      p1[mt][0] = p1[mt][1] = 0.0;
+      p2[mt][0] = p2[mt][1] = 0.0;
+      p3[mt][0] = p3[mt][1] = 0.0;
+    }
+#pragma unroll 4
+    for (int ks = 0; ks < 16; ++ks) {
+      const double2 xb = X[(ks * 4 + (lane & 3)) * 8 + (lane >> 2)];
+      const double xs = xb.x + xb.y;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const double2 s = sS[(mt * 16 + ks) * 32 + lane];
+        dmma(p1[mt][0], p1[mt][1], s.x, xb.x);
+        dmma(p2[mt][0], p2[mt][1], s.y, xb.y);
+        dmma(p3[mt][0], p3[mt][1], s.x + s.y, xs);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int row = mt * 8 + (lane >> 2), col = 2 * (lane & 3);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double yr = p1[mt][c] - p2[mt][c];
+        double yi = p3[mt][c] - p1[mt][c] - p2[mt][c];
+        X[row * 8 + col + c] = make_double2(yr, yi);
+      }
+    }
+    __syncwarp();
+    {
+      uint64_t t = tile * 8 + ld_t;
+      if (t < p.n_tuples) {
+        uint64_t base = insert_zeros(t, p.lo_mask, 6);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          int m = ld_m0 + 4 * i;
+          a[base + sOff[m]] = X[m * 8 + ld_t];
+        }
+      }
+    }
+    __syncwarp();
+    cur ^= 1;
+  }
+}
+
+static size_t gate3_smem_bytes() {
+  return 4096 * sizeof(double2) + (size_t)k3Warps * 2 * 512 * sizeof(double2) + 64 * 8;
+}
+
+cudaError_t launch_gate3(double2* a, const Gate3Params& p, cudaStream_t st) {
+  static bool attr_set = false;
+  size_t smem = gate3_smem_bytes();
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gate3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t tiles = (p.n_tuples + 7) / 8;
+  uint64_t ctas = (tiles + k3Warps - 1) / k3Warps;
+  unsigned grid = (unsigned)(ctas < (uint64_t)sms ? ctas : (uint64_t)sms);
+  if (grid < 1) grid = 1;
+  gate3_kernel<<<grid, k3Warps * 32, smem, st>>>(a, p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// state init, remap
+// ------------------------------------------------------------------------------------
+__global__ void set_one_kernel(double2* a) { a[0] = make_double2(1.0, 0.0); }
+
+cudaError_t launch_init(double2* a, uint64_t elems, bool one_at_zero, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a, 0, elems * sizeof(double2), st);
+  if (e != cudaSuccess) return e;
+  if (one_at_zero) set_one_kernel<<<1, 1, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void swap_halves_kernel(double2* __restrict__ A, double2* __restrict__ B, uint64_t half,
+                                   int b, int va, int vb) {
+  const uint64_t lowmask = ((uint64_t)1 << b) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < half; e += stride) {
+    uint64_t hi = (e >> b) << (b + 1), lo = e & lowmask;
+    uint64_t oa = hi | ((uint64_t)va << b) | lo;
+    uint64_t ob = hi | ((uint64_t)vb << b) | lo;
+    double2 x = A[oa], y = B[ob];
+    A[oa] = y;
+    B[ob] = x;
+  }
+}
+
+cudaError_t launch_swap_halves(double2* A, double2* B, int L, int b, int va, int vb,
+                               cudaStream_t st) {
+  uint64_t half = (uint64_t)1 << (L - 1);
+  swap_halves_kernel<<<grid_for(half, kThreads, 148ull * 32), kThreads, 0, st>>>(A, B, half, b, va,
+                                                                               vb);
+  return cudaGetLastError();
+}
+
+__global__ void pack_kernel(const double2* __restrict__ a, double2* __restrict__ buf, int b, int v,
+                            uint64_t first, uint64_t count, int dir) {
+  const uint64_t lowmask = ((uint64_t)1 << b) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t e = first + i;
+    uint64_t o = ((e >> b) << (b + 1)) | ((uint64_t)v << b) | (e & lowmask);
+    if (dir == 0)
+      buf[i] = a[o];
+    else
+      const_cast<double2*>(a)[o] = buf[i];
+  }
+}
+
+cudaError_t launch_pack_half(const double2* a, double2* buf, int b, int v, uint64_t first,
+                             uint64_t count, cudaStream_t st) {
+  pack_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(a, buf, b, v, first,
+                                                                          count, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack_half(double2* a, const double2* buf, int b, int v, uint64_t first,
+                               uint64_t count, cudaStream_t st) {
+  pack_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, const_cast<double2*>(buf), b, v, first, count, 1);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// vec(rho) order <-> physical order
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t vec_to_phys(uint64_t v, const BitMap& bm, int n) {
+  // v = r + c 2^n; logical bit 2q = r_q, 2q+1 = c_q
+  uint64_t P = 0;
+  for (int q = 0; q < n; ++q) {
+    P |= ((v >> q) & 1ull) << bm.phys[2 * q];
+    P |= ((v >> (n + q)) & 1ull) << bm.phys[2 * q + 1];
+  }
+  return P;
+}
+
+__global__ void gather_vec_kernel(const double2* __restrict__ a, double2* __restrict__ out,
+                                  const __grid_constant__ BitMap bm, int n, int L, uint64_t shard,
+                                  uint64_t first, uint64_t count, int zero_unowned) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lmask = ((uint64_t)1 << L) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t P = vec_to_phys(first + i, bm, n);
+    if ((P >> L) == shard)
+      out[i] = a[P & lmask];
+    else if (zero_unowned)
+      out[i] = make_double2(0.0, 0.0);
+  }
+}
+
+__global__ void scatter_vec_kernel(double2* __restrict__ a, const double2* __restrict__ in,
+                                   const __grid_constant__ BitMap bm, int n, int L, uint64_t shard,
+                                   uint64_t first, uint64_t count) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lmask = ((uint64_t)1 << L) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t P = vec_to_phys(first + i, bm, n);
+    if ((P >> L) == shard) a[P & lmask] = in[i];
+  }
+}
+
+cudaError_t launch_gather_vec(const double2* a, double2* out, const BitMap& bm, int n, int L,
+                              uint64_t shard, uint64_t first, uint64_t count, bool zero_unowned,
+                              cudaStream_t st) {
+  gather_vec_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, out, bm, n, L, shard, first, count, zero_unowned ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_vec(double2* a, const double2* in, const BitMap& bm, int n, int L,
+                               uint64_t shard, uint64_t first, uint64_t count, cudaStream_t st) {
+  scatter_vec_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, in, bm, n, L, shard, first, count);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// diagonal reductions (A-7)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t diag_phys(uint64_t x, const BitMap& bm, int n) {
+  uint64_t P = 0;
+  for (int q = 0; q < n; ++q) {
+    uint64_t b = (x >> q) & 1ull;
+    P |= (b << bm.phys[2 * q]) | (b << bm.phys[2 * q + 1]);
+  }
+  return P;
+}
+
+__global__ void diag_kernel(const double2* __restrict__ a, double* __restrict__ probs,
+                            unsigned long long* imax, const __grid_constant__ BitMap bm, int n,
+                            int L, uint64_t shard) {
+  const uint64_t N = (uint64_t)1 << n;
+  const uint64_t lmask = ((uint64_t)1 << L) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double mi = 0.0;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < N; x += stride) {
+    uint64_t P = diag_phys(x, bm, n);
+    if ((P >> L) != shard) continue;
+    double2 v = a[P & lmask];
+    probs[x] = v.x;
+    mi = fmax(mi, fabs(v.y));
+  }
+  if (mi > 0.0) atomicMax(imax, (unsigned long long)__double_as_longlong(mi));
+}
+
+cudaError_t launch_diag(const double2* a, double* probs, unsigned long long* imax,
+                        const BitMap& bm, int n, int L, uint64_t shard, cudaStream_t st) {
+  uint64_t N = (uint64_t)1 << n;
+  diag_kernel<<<grid_for(N, kThreads, 148ull * 8), kThreads, 0, st>>>(a, probs, imax, bm, n, L,
+                                                                     shard);
+  return cudaGetLastError();
+}
+
+__global__ void readout_kernel(double* p, uint64_t half, int q, double p10, double p01) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lo = ((uint64_t)1 << q) - 1;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < half; e += stride) {
+    uint64_t x0 = ((e & ~lo) << 1) | (e & lo), x1 = x0 | ((uint64_t)1 << q);
+    double a0 = p[x0], a1 = p[x1];
+    p[x0] = (1.0 - p10) * a0 + p01 * a1;
+    p[x1] = p10 * a0 + (1.0 - p01) * a1;
+  }
+}
+
+cudaError_t launch_readout(double* p, int n, const double* p10, const double* p01,
+                           cudaStream_t st) {
+  uint64_t half = (uint64_t)1 << (n - 1);
+  for (int q = 0; q < n; ++q) {
+    double a = p10 ? p10[q] : 0.0, b = p01 ? p01[q] : 0.0;
+    if (a == 0.0 && b == 0.0) continue;
+    readout_kernel<<<grid_for(half, kThreads, 148ull * 8), kThreads, 0, st>>>(p, half, q, a, b);
+  }
+  return cudaGetLastError();
+}
+
+int expect_blocks(int n) {
+  uint64_t N = (uint64_t)1 << n;
+  uint64_t b = (N + kThreads * 8 - 1) / (kThreads * 8);
+  if (b > 148 * 4) b = 148 * 4;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+__device__ __forceinline__ double2 block_sum2(double2 v) {
+  __shared__ double2 red[kThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      s.x += red[i].x;
+      s.y += red[i].y;
+    }
+  return s;
+}
+
+// tr(P rho) = (-i)^{popc(x&z)} sum_a (-1)^{popc(a&z)} rho[a^x][a]   (A-7)
+__global__ void expect_kernel(const double2* __restrict__ a, double2* partial,
+                              const __grid_constant__ BitMap bm, int n, int L, uint64_t shard,
+                              uint64_t xm, uint64_t zm) {
+  const uint64_t N = (uint64_t)1 << n;
+  const uint64_t lmask = ((uint64_t)1 << L) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double2 acc = make_double2(0.0, 0.0);
+  for (uint64_t col = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; col < N; col += stride) {
+    uint64_t row = col ^ xm;
+    uint64_t P = 0;
+    for (int q = 0; q < n; ++q) {
+      P |= ((row >> q) & 1ull) << bm.phys[2 * q];
+      P |= ((col >> q) & 1ull) << bm.phys[2 * q + 1];
+    }
+    if ((P >> L) != shard) continue;
+    double2 v = a[P & lmask];
+    double sgn = (__popcll(col & zm) & 1) ? -1.0 : 1.0;
+    acc.x += sgn * v.x;
+    acc.y += sgn * v.y;
+  }
+  double2 s = block_sum2(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+cudaError_t launch_expect(const double2* a, double2* partial, int nblocks, const BitMap& bm,
+                          int n, int L, uint64_t shard, uint64_t xm, uint64_t zm,
+                          cudaStream_t st) {
+  expect_kernel<<<nblocks, kThreads, 0, st>>>(a, partial, bm, n, L, shard, xm, zm);
+  return cudaGetLastError();
+}
+
+__global__ void reduce_partials_kernel(const double2* partial, int nb, double2* out) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    acc.x += partial[i].x;
+    acc.y += partial[i].y;
+  }
+  double2 s = block_sum2(acc);
+  if (threadIdx.x == 0) *out = s;
+}
+
+cudaError_t launch_reduce_partials(const double2* partial, int nblocks, double2* out,
+                                   cudaStream_t st) {
+  reduce_partials_kernel<<<1, kThreads, 0, st>>>(partial, nblocks, out);
+  return cudaGetLastError();
+}
+
+__global__ void add_kernel(double* dst, const double* src, uint64_t count) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride)
+    dst[i] += src[i];
+}
+cudaError_t launch_add(double* dst, const double* src, uint64_t count, cudaStream_t st) {
+  add_kernel<<<grid_for(count, kThreads, 148ull * 8), kThreads, 0, st>>>(dst, src, count);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// sampling: clamp + scan (one CTA), Philox4x32-10 + binary search
+// ------------------------------------------------------------------------------------
+__global__ void cdf_kernel(const double* __restrict__ p, double* __restrict__ cdf, uint64_t N) {
+  __shared__ double part[1024];
+  const uint64_t per = (N + blockDim.x - 1) / blockDim.x;
+  const uint64_t b0 = threadIdx.x * per, b1 = min(N, b0 + per);
+  double s = 0.0;
+  for (uint64_t i = b0; i < b1; ++i) s += fmax(p[i], 0.0);
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double run = 0.0;
+    for (unsigned i = 0; i < blockDim.x; ++i) {
+      double v = part[i];
+      part[i] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  double run = part[threadIdx.x];
+  for (uint64_t i = b0; i < b1; ++i) {
+    run += fmax(p[i], 0.0);
+    cdf[i] = run;
+  }
+}
+
+cudaError_t launch_cdf(const double* p, double* cdf, int n, cudaStream_t st) {
+  cdf_kernel<<<1, 1024, 0, st>>>(p, cdf, (uint64_t)1 << n);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ void philox_round(uint32_t c[4], const uint32_t k[2]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  uint32_t hi0 = __umulhi(M0, c[0]), lo0 = M0 * c[0];
+  uint32_t hi1 = __umulhi(M1, c[2]), lo1 = M1 * c[2];
+  uint32_t n0 = hi1 ^ c[1] ^ k[0], n1 = lo1, n2 = hi0 ^ c[3] ^ k[1], n3 = lo0;
+  c[0] = n0;
+  c[1] = n1;
+  c[2] = n2;
+  c[3] = n3;
+}
+
+__device__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  uint32_t k[2] = {k0, k1};
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    philox_round(c, k);
+    k[0] += 0x9E3779B9u;
+    k[1] += 0xBB67AE85u;
+  }
+}
+
+__global__ void sample_kernel(const double* __restrict__ cdf, uint64_t N, uint64_t seed,
+                              uint64_t shots, unsigned long long* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const double total = cdf[N - 1];
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < shots; s += stride) {
+    uint32_t c[4] = {(uint32_t)s, (uint32_t)(s >> 32), 0u, 0u};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    uint64_t bits = ((uint64_t)c[0] << 21) ^ ((uint64_t)c[1] >> 11);  // 53 random bits
+    double u = (double)(bits & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0);
+    double target = u * total;
+    uint64_t lo = 0, hi = N - 1;  // first index with cdf > target
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (cdf[mid] > target)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    out[s] = lo;
+  }
+}
+
+cudaError_t launch_sample(const double* cdf, int n, uint64_t seed, uint64_t shots,
+                          unsigned long long* out, cudaStream_t st) {
+  sample_kernel<<<grid_for(shots, kThreads, 148ull * 8), kThreads, 0, st>>>(
+      cdf, (uint64_t)1 << n, seed, shots, out);
+  return cudaGetLastError();
+}
+
+}  // namespace tanq

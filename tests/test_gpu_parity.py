@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bar (BASELINE.json north star): max |delta rho_ij| <= 1e-10 and
+||delta rho||_F / ||rho_oracle||_F <= 1e-12, same bound for probabilities and expectations.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import dense, statevector
+
+pytestmark = pytest.mark.gpu
+
+ABS, REL = 1e-10, 1e-12
+
+
+@pytest.fixture(scope="module")
+def Sim():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from __graft_entry__ import build
+    build()
+    from paper_2404_13184_b200 import Simulator
+    return Simulator
+
+
+def rho_of(sim, n):
+    N = 2 ** n
+    return sim.get_state().reshape(N, N).T
+
+
+def assert_parity(got, ref, abs_tol=ABS, rel_tol=REL):
+    d = got - ref
+    mx = np.abs(d).max()
+    rel = np.linalg.norm(d) / np.linalg.norm(ref)
+    assert mx <= abs_tol and rel <= rel_tol, f"max abs {mx:.3e}, rel Frobenius {rel:.3e}"
+
+
+# --------------------------------------------------------------------------------------
+# config 1: GHZ-3 worked example
+# --------------------------------------------------------------------------------------
+
+def test_ghz3_worked_example(Sim):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ghz3.json")))
+    c, nm = W.config_workload(1)
+    for fuse in (0, 1, 2):
+        with Sim(3) as sim:
+            sim.run_circuit(c, nm, fuse=fuse)
+            rho = rho_of(sim, 3)
+            assert_parity(rho, dense.run(c, nm))
+            np.testing.assert_allclose(np.diag(rho).real, g["diag"], atol=1e-15)
+            assert abs(rho[0, 7] - g["rho_0_7"]) < 1e-15
+            p = sim.probs(dense.readout_of(nm))
+            np.testing.assert_allclose(p, g["readout_probs"], atol=g["readout_tolerance"])
+    with Sim(3) as sim:
+        sim.run_circuit(c)
+        np.testing.assert_allclose(sim.probs(), g["noiseless_diag"], atol=1e-15)
+        s1 = sim.sample(500, seed=7)
+        s2 = sim.sample(500, seed=7)
+        assert (s1 == s2).all()                      # reproducible per seed
+        assert set(np.unique(s1)) <= {0, 7}
+        assert abs((s1 == 0).sum() - 250) < 5 * math.sqrt(125)
+
+
+def test_sampling_statistics(Sim):
+    c, nm = W.config_workload(1)
+    with Sim(3) as sim:
+        sim.run_circuit(c, nm)
+        ro = dense.readout_of(nm)
+        p = sim.probs(ro)
+        shots = 200000
+        s = sim.sample(shots, seed=123, readout=ro)
+        counts = np.bincount(s.astype(np.int64), minlength=8)
+        sigma = np.sqrt(shots * p * (1 - p))
+        assert (np.abs(counts - shots * p) <= 5 * sigma + 1).all()
+
+
+# --------------------------------------------------------------------------------------
+# raw entry points on random states, every kernel variant
+# --------------------------------------------------------------------------------------
+
+def _random_state(rng, n):
+    return W.random_density(rng, n, rank=4)
+
+
+@pytest.mark.parametrize("n,qubits", [
+    (1, (0,)), (3, (0,)), (3, (2,)), (5, (1,)), (6, (5,)),        # k=1, pair / strided
+    (2, (0, 1)), (4, (1, 0)), (4, (3, 0)), (6, (2, 4)), (7, (6, 5)),  # k=2
+    (3, (0, 1, 2)), (5, (4, 0, 2)), (6, (1, 3, 5)), (8, (7, 2, 4)), (9, (0, 8, 3)),  # k=3
+])
+def test_apply_superop_random(Sim, n, qubits):
+    rng = np.random.default_rng(n * 100 + sum(qubits))
+    k = len(qubits)
+    rho = _random_state(rng, n)
+    S = W.random_complex(rng, (4 ** k, 4 ** k)) * 0.3
+    with Sim(n) as sim:
+        sim.set_state(dense.to_vec(rho))
+        sim.apply_superop(qubits, S)
+        got = rho_of(sim, n)
+    ref = np.ascontiguousarray(rho.copy())
+    dense.apply_superop(ref, n, qubits, S)
+    assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("n,qubits", [(3, (1,)), (4, (0, 3)), (5, (2, 1, 4)), (7, (6,))])
+def test_apply_gate_and_channel(Sim, n, qubits):
+    rng = np.random.default_rng(7 + n)
+    k = len(qubits)
+    rho = _random_state(rng, n)
+    U = W.random_unitary(rng, 2 ** k)
+    Ks = W.random_kraus(rng, 2 ** k, 3)
+    with Sim(n) as sim:
+        sim.set_state(dense.to_vec(rho))
+        sim.apply_gate(qubits, U)
+        sim.apply_channel(qubits, Ks, check_cptp=True)
+        got = rho_of(sim, n)
+    ref = np.ascontiguousarray(rho.copy())
+    dense.apply_kraus(ref, n, qubits, [U])
+    dense.apply_kraus(ref, n, qubits, Ks)
+    assert_parity(got, ref)
+
+
+# --------------------------------------------------------------------------------------
+# circuits with noise, fusion modes, shards
+# --------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("fuse,kmax", [(0, 2), (1, 2), (2, 2), (2, 3)])
+def test_random_noisy_circuits(Sim, seed, fuse, kmax):
+    n = 3 + seed
+    c = W.random_circuit(n, 50, seed=500 + seed, kmax=3)
+    nm = W.synthetic_calibration(c, seed, depol=True, thermal=True, overrot=True)
+    nm.order = seed % 2
+    with Sim(n) as sim:
+        sim.run_circuit(c, nm, fuse=fuse, k_max=kmax)
+        got = rho_of(sim, n)
+    assert_parity(got, dense.run(c, nm))
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+@pytest.mark.parametrize("seed", range(3))
+def test_virtual_shards_remap(Sim, shards, seed):
+    """Shards on one device: global-bit remaps (A-6) must leave the result unchanged."""
+    n = 5 + seed
+    c = W.random_circuit(n, 60, seed=700 + seed, kmax=3)
+    nm = W.synthetic_calibration(c, seed, depol=True, thermal=True)
+    ref = dense.run(c, nm)
+    with Sim(n, shards) as sim:
+        st = sim.run_circuit(c, nm, fuse=2, k_max=3)
+        got = rho_of(sim, n)
+        assert st["n_remaps"] > 0
+        p = sim.probs(dense.readout_of(nm))
+        e = sim.expect_pauli(0b101, 0b110)
+    assert_parity(got, ref)
+    np.testing.assert_allclose(p, dense.probs(ref, n, dense.readout_of(nm)), atol=ABS)
+    assert abs(e - dense.expect_pauli(ref, n, 0b101, 0b110)) < ABS
+
+
+def test_config2_qft10_thermal_overrotation(Sim):
+    c, nm = W.config_workload(2)
+    ref = dense.run(c, nm)
+    for fuse, kmax in ((1, 2), (2, 2), (2, 3)):
+        with Sim(10) as sim:
+            sim.run_circuit(c, nm, fuse=fuse, k_max=kmax)
+            assert_parity(rho_of(sim, 10), ref)
+
+
+def test_config2_qft_noiseless_closed_form(Sim):
+    n = 10
+    c = W.qft_circuit(n, x=613)
+    with Sim(n) as sim:
+        sim.run_circuit(c)
+        rho = rho_of(sim, n)
+    r = np.arange(2 ** n)
+    closed = np.exp(2j * math.pi * 613 * (r[:, None] - r[None, :]) / 2 ** n) / 2 ** n
+    assert np.abs(rho - closed).max() < 1e-12
+
+
+def test_config3_scaled_random_layered(Sim):
+    c, nm = W.config_workload(3, n=9, depth=12)
+    ref = dense.run(c, nm)
+    for kmax in (2, 3):
+        with Sim(9) as sim:
+            sim.run_circuit(c, nm, fuse=2, k_max=kmax)
+            assert_parity(rho_of(sim, 9), ref)
+
+
+def test_config4_scaled_qpe(Sim):
+    c, nm = W.config_workload(4, n=8)
+    ref = dense.run(c, nm)
+    for shards in (1, 2, 4):
+        with Sim(8, shards) as sim:
+            sim.run_circuit(c, nm)
+            assert_parity(rho_of(sim, 8), ref)
+            np.testing.assert_allclose(sim.probs(dense.readout_of(nm)),
+                                       dense.probs(ref, 8, dense.readout_of(nm)), atol=ABS)
+
+
+def test_config5_scaled_vqe_expectations(Sim):
+    c, nm = W.config_workload(5, n=7)
+    ref = dense.run(c, nm)
+    for shards in (1, 8):
+        with Sim(7, shards) as sim:
+            sim.run_circuit(c, nm)
+            for xm, zm in c.paulis:
+                e = sim.expect_pauli(xm, zm)
+                r = dense.expect_pauli(ref, 7, xm, zm)
+                assert abs(e.real - r.real) < ABS and abs(e.imag) < ABS
+
+
+# --------------------------------------------------------------------------------------
+# edge cases and errors
+# --------------------------------------------------------------------------------------
+
+def test_empty_circuit_and_reset(Sim):
+    with Sim(4) as sim:
+        sim.run_circuit(W.Circuit(4, []))
+        p = sim.probs()
+        assert p[0] == 1.0 and p[1:].sum() == 0.0
+        sim.run_circuit(W.Circuit(4, [W.Op("x", (2,))]))
+        sim.reset()
+        assert sim.probs()[0] == 1.0
+
+
+def test_argument_errors(Sim):
+    from paper_2404_13184_b200 import TanqError
+    with Sim(3) as sim:
+        for bad in ([W.Op("x", (3,))], [W.Op("cx", (1, 1))]):
+            with pytest.raises(TanqError) as e:
+                sim.run_circuit(W.Circuit(3, bad))
+            assert e.value.status == 1
+        nm = W.NoiseModel(3, [W.QubitCal(10.0, 25.0) for _ in range(3)])
+        nm.gates[("x", (0,))] = W.GateCal(0.0, 10.0)
+        with pytest.raises(TanqError):
+            sim.run_circuit(W.Circuit(3, [W.Op("x", (0,))]), nm)      # T2 > 2 T1
+        nm = W.NoiseModel(3, [W.QubitCal() for _ in range(3)])
+        with pytest.raises(TanqError):
+            sim.run_circuit(W.Circuit(3, [W.Op("sx", (1,))]), nm)     # missing calibration
+        with pytest.raises(TanqError):
+            sim.apply_channel((0,), [np.eye(2) * 0.5], check_cptp=True)
+        # state untouched by the rejected calls
+        assert sim.probs()[0] == 1.0
+
+
+def test_noiseless_purity_statevector(Sim):
+    for n in (6, 9):
+        c = W.random_layered(n, 6, seed=n)
+        psi = statevector.run(c)
+        with Sim(n) as sim:
+            sim.run_circuit(c, fuse=2, k_max=3)
+            assert np.abs(rho_of(sim, n) - np.outer(psi, psi.conj())).max() < 1e-12

@@ -201,7 +201,8 @@ def run_ours(args):
         sim = Simulator(n, world_size=world, rank=rank, device=local, nccl_uid=uid[0])
     else:
         sim = Simulator(n, 1)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()          # a real stream: events on it bracket the kernels
+    torch.cuda.set_stream(stream)
     sim.set_stream(stream.cuda_stream)
     ro = CReadout.of(nm)
     plan = Plan(sim, c, nm, fuse=args.fuse, k_max=args.kmax, profile=True)

@@ -212,6 +212,11 @@ tanq_status tanq_plan_create_host(int n_qubits, int world_size, const tanq_circu
                                   tanq_plan** out);
 /* ops_in, ops_fused, n_k[] and plan_ms of a plan (n_remaps / remap_bytes are 0). */
 tanq_status tanq_plan_info(const tanq_plan* p, tanq_run_stats* st);
+/* Execution schedule of a plan on world_size shards, as the engine runs it: items of three
+ * int32 {kind, x, y}; kind 0 = fused op x; kind 1 = remap swapping physical bit x (global)
+ * with local bit y (A-6).  Pass items = NULL to query the count. */
+tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* items, uint64_t max,
+                               uint64_t* n_items);
 /* Fused op i: arity, qubits (k ints) and, if S != NULL, its 4^k x 4^k superoperator in the
  * paper's vec convention (local index r + c 2^k over qubits[0..k-1]). */
 tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits, tanq_c64* S);

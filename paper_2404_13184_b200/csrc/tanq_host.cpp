@@ -435,6 +435,10 @@ struct tanq_sim {
   uint64_t launches = 0;
   uint64_t remap_count = 0, remap_bytes = 0;
   std::vector<std::pair<int, cudaStream_t>> owned;  // library-created stream per device
+  double2* frag_host = nullptr;                      // pinned staging of k=3 fragments
+  size_t frag_host_elems = 0;
+  cudaEvent_t frag_done = nullptr;
+  bool frag_done_pending = false;
   cudaStream_t own_streams_of(int dev) const {
     for (auto& p : owned)
       if (p.first == dev) return p.second;
@@ -547,46 +551,73 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
   return TANQ_OK;
 }
 
-// Make every target bit of (k, q) local; victims = local bits not targeted, whose qubit is
-// used furthest in the future (lookahead over `next`), ties to the highest position.
-tanq_status ensure_local(tanq_sim* s, int k, const int* q, const std::vector<FusedOp>* next,
-                         size_t next_from) {
-  const int L = s->L;
-  std::vector<int> tgt;
-  for (int j = 0; j < k; ++j) {
-    tgt.push_back(2 * q[j]);
-    tgt.push_back(2 * q[j] + 1);
-  }
-  for (int id : tgt) {
-    const int a = (int)s->phys[id];
-    if (a < L) continue;
-    int best = -1;
-    long best_dist = -1;
-    for (int b = L - 1; b >= 0; --b) {
-      int lid = -1;
-      for (int i = 0; i < 2 * s->n; ++i)
-        if (s->phys[i] == (uint32_t)b) lid = i;
-      if (std::find(tgt.begin(), tgt.end(), lid) != tgt.end()) continue;
-      const int lq = lid / 2;
-      long dist = 1L << 40;
-      if (next) {
-        for (size_t t = next_from; t < next->size() && t < next_from + 256; ++t) {
-          const FusedOp& f = (*next)[t];
-          bool uses = false;
-          for (int j = 0; j < f.k; ++j) uses |= f.q[j] == lq;
-          if (uses) {
-            dist = (long)(t - next_from);
-            break;
-          }
+// Victim for a remap (pure layout logic, shared by execution and tanq_plan_schedule): a local
+// bit not targeted by the op whose qubit is used furthest in the future (lookahead 256 ops
+// over `next` from `next_from`), ties to the highest position.  -1 if none.
+int choose_victim(const uint32_t* phys, int n, int L, const std::vector<int>& tgt,
+                  const std::vector<FusedOp>* next, size_t next_from) {
+  int best = -1;
+  long best_dist = -1;
+  for (int b = L - 1; b >= 0; --b) {
+    int lid = -1;
+    for (int i = 0; i < 2 * n; ++i)
+      if (phys[i] == (uint32_t)b) lid = i;
+    if (std::find(tgt.begin(), tgt.end(), lid) != tgt.end()) continue;
+    const int lq = lid / 2;
+    long dist = 1L << 40;
+    if (next) {
+      for (size_t t = next_from; t < next->size() && t < next_from + 256; ++t) {
+        const FusedOp& f = (*next)[t];
+        bool uses = false;
+        for (int j = 0; j < f.k; ++j) uses |= f.q[j] == lq;
+        if (uses) {
+          dist = (long)(t - next_from);
+          break;
         }
       }
-      if (dist > best_dist) {
-        best_dist = dist;
-        best = b;
-      }
     }
-    if (best < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
-    TRY(remap_swap(s, a, best));
+    if (dist > best_dist) {
+      best_dist = dist;
+      best = b;
+    }
+  }
+  return best;
+}
+
+// The remaps (a global, b local) that make op `op` local, applied to `phys` in order.
+std::vector<std::pair<int, int>> plan_remaps(uint32_t* phys, int n, int L, const FusedOp& op,
+                                             const std::vector<FusedOp>* next, size_t next_from) {
+  std::vector<std::pair<int, int>> out;
+  std::vector<int> tgt;
+  for (int j = 0; j < op.k; ++j) {
+    tgt.push_back(2 * op.q[j]);
+    tgt.push_back(2 * op.q[j] + 1);
+  }
+  for (int id : tgt) {
+    const int a = (int)phys[id];
+    if (a < L) continue;
+    const int b = choose_victim(phys, n, L, tgt, next, next_from);
+    if (b < 0) return {{-1, -1}};
+    out.push_back({a, b});
+    for (int i = 0; i < 2 * n; ++i) {
+      if (phys[i] == (uint32_t)a)
+        phys[i] = (uint32_t)b;
+      else if (phys[i] == (uint32_t)b)
+        phys[i] = (uint32_t)a;
+    }
+  }
+  return out;
+}
+
+// Make every target bit of `op` local on the device (remap_swap per planned swap).
+tanq_status ensure_local(tanq_sim* s, const FusedOp& op, const std::vector<FusedOp>* next,
+                         size_t next_from) {
+  uint32_t phys[64];
+  std::memcpy(phys, s->phys, sizeof(phys));
+  auto swaps = plan_remaps(phys, s->n, s->L, op, next, next_from);
+  for (auto& ab : swaps) {
+    if (ab.first < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
+    TRY(remap_swap(s, ab.first, ab.second));
   }
   return TANQ_OK;
 }
@@ -702,74 +733,80 @@ tanq_status ensure_frag_capacity(tanq_sim* s, DevScratch& d, size_t elems) {
 
 // Execute a list of fused ops in order (remaps inserted as needed).
 tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
-  // k=3 fragment staging: fragments depend on the layout at execution time, so they are
-  // built op by op into a pinned host ring and copied to each device before the launch.
+  // k=3 fragments depend on the layout at execution time, so they are built op by op into a
+  // persistent pinned host buffer and copied (async) to each device before the launch.
   size_t n3 = 0;
   for (const auto& op : ops) n3 += op.k == 3;
   const size_t fe = tanq::gate3_frag_elems();
-  double2* pinned = nullptr;
   if (n3) {
     for (auto& sh : s->shards) {
       DevScratch& d = scratch_for(s, sh.device);
       TRY(ensure_scratch(s, d));
       TRY(ensure_frag_capacity(s, d, fe * n3));
     }
-    CUDA_TRY(cudaMallocHost(&pinned, fe * n3 * sizeof(double2)));
-  }
-  size_t i3 = 0;
-  tanq_status st = TANQ_OK;
-  for (size_t i = 0; i < ops.size() && st == TANQ_OK; ++i) {
-    const FusedOp& op = ops[i];
-    st = ensure_local(s, op.k, op.q, &ops, i + 1);
-    if (st != TANQ_OK) break;
-    if (op.k == 3) {
-      std::vector<std::pair<int, int>> bits;
-      for (int j = 0; j < 3; ++j) {
-        bits.push_back({(int)s->phys[2 * op.q[j]], j});
-        bits.push_back({(int)s->phys[2 * op.q[j] + 1], 3 + j});
-      }
-      std::sort(bits.begin(), bits.end());
-      std::vector<double2> Sm(64 * 64);
-      int l_of[64];
-      for (int m = 0; m < 64; ++m) {
-        int l = 0;
-        for (int t = 0; t < 6; ++t)
-          if ((m >> t) & 1) l |= 1 << bits[t].second;
-        l_of[m] = l;
-      }
-      for (int a = 0; a < 64; ++a)
-        for (int b = 0; b < 64; ++b) {
-          cd v = op.S(l_of[a], l_of[b]);
-          Sm[a * 64 + b] = make_double2(v.real(), v.imag());
-        }
-      double2* hf = pinned + fe * i3;
-      tanq::gate3_make_frags(Sm.data(), hf);
-      std::vector<const double2*> ptrs(s->scratch.size(), nullptr);
-      for (auto& sh : s->shards) {
-        DevScratch& d = scratch_for(s, sh.device);
-        int di = 0;
-        for (size_t q = 0; q < s->scratch.size(); ++q)
-          if (s->scratch[q].device == sh.device) di = (int)q;
-        double2* dst = d.frag + fe * i3;
-        if (!ptrs[di]) {
-          CUDA_TRY(cudaSetDevice(sh.device));
-          CUDA_TRY(cudaMemcpyAsync(dst, hf, fe * sizeof(double2), cudaMemcpyHostToDevice,
-                                   sh.stream));
-          ptrs[di] = dst;
-        }
-      }
-      ++i3;
-      st = launch_op(s, op, &ptrs);
-    } else {
-      st = launch_op(s, op, nullptr);
+    if (s->frag_done_pending) {  // previous H2D copies from the pinned buffer must be done
+      CUDA_TRY(cudaEventSynchronize(s->frag_done));
+      s->frag_done_pending = false;
+    }
+    if (s->frag_host_elems < fe * n3) {
+      if (s->frag_host) CUDA_TRY(cudaFreeHost(s->frag_host));
+      CUDA_TRY(cudaMallocHost(&s->frag_host, fe * n3 * sizeof(double2)));
+      s->frag_host_elems = fe * n3;
     }
   }
-  if (pinned) {
-    tanq_status js = join_all(s);
-    cudaFreeHost(pinned);
-    if (st == TANQ_OK) st = js;
+  size_t i3 = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const FusedOp& op = ops[i];
+    TRY(ensure_local(s, op, &ops, i + 1));
+    if (op.k != 3) {
+      TRY(launch_op(s, op, nullptr));
+      continue;
+    }
+    std::vector<std::pair<int, int>> bits;
+    for (int j = 0; j < 3; ++j) {
+      bits.push_back({(int)s->phys[2 * op.q[j]], j});
+      bits.push_back({(int)s->phys[2 * op.q[j] + 1], 3 + j});
+    }
+    std::sort(bits.begin(), bits.end());
+    std::vector<double2> Sm(64 * 64);
+    int l_of[64];
+    for (int m = 0; m < 64; ++m) {
+      int l = 0;
+      for (int t = 0; t < 6; ++t)
+        if ((m >> t) & 1) l |= 1 << bits[t].second;
+      l_of[m] = l;
+    }
+    for (int a = 0; a < 64; ++a)
+      for (int b = 0; b < 64; ++b) {
+        cd v = op.S(l_of[a], l_of[b]);
+        Sm[a * 64 + b] = make_double2(v.real(), v.imag());
+      }
+    double2* hf = s->frag_host + fe * i3;
+    tanq::gate3_make_frags(Sm.data(), hf);
+    std::vector<const double2*> ptrs(s->scratch.size(), nullptr);
+    for (auto& sh : s->shards) {
+      int di = 0;
+      for (size_t q = 0; q < s->scratch.size(); ++q)
+        if (s->scratch[q].device == sh.device) di = (int)q;
+      if (!ptrs[di]) {
+        double2* dst = s->scratch[di].frag + fe * i3;
+        CUDA_TRY(cudaSetDevice(sh.device));
+        CUDA_TRY(cudaMemcpyAsync(dst, hf, fe * sizeof(double2), cudaMemcpyHostToDevice, sh.stream));
+        ptrs[di] = dst;
+      }
+    }
+    ++i3;
+    TRY(launch_op(s, op, &ptrs));
   }
-  return st;
+  if (n3) {
+    Shard& s0 = s->shards[0];
+    for (auto& sh : s->shards) TRY(stream_wait(s0, sh));
+    CUDA_TRY(cudaSetDevice(s0.device));
+    if (!s->frag_done) CUDA_TRY(cudaEventCreateWithFlags(&s->frag_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(s->frag_done, s0.stream));
+    s->frag_done_pending = true;
+  }
+  return TANQ_OK;
 }
 
 tanq_status check_qubits(const tanq_sim* s, int k, const int* q) {
@@ -1126,6 +1163,8 @@ tanq_status tanq_destroy(tanq_sim* s) {
     cudaFree(d.stage);
     cudaFree(d.frag);
   }
+  if (s->frag_host) cudaFreeHost(s->frag_host);
+  if (s->frag_done) cudaEventDestroy(s->frag_done);
   if (s->xsend) cudaFree(s->xsend);
   if (s->xrecv) cudaFree(s->xrecv);
   if (s->comm) nccl().CommDestroy(s->comm);
@@ -1296,6 +1335,35 @@ tanq_status tanq_plan_info(const tanq_plan* p, tanq_run_stats* st) {
   st->ops_fused = p->ops.size();
   for (const auto& f : p->ops) st->n_k[f.k]++;
   st->plan_ms = p->plan_ms;
+  return TANQ_OK;
+}
+
+tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* items, uint64_t max,
+                               uint64_t* n_items) {
+  if (!p || !n_items) return fail(TANQ_E_ARG, "NULL argument");
+  if (world_size != 1 && world_size != 2 && world_size != 4 && world_size != 8)
+    return fail(TANQ_E_ARG, "world_size must be 1, 2, 4 or 8");
+  const int L = 2 * p->n - ilog2(world_size);
+  uint32_t phys[64];
+  for (int i = 0; i < 64; ++i) phys[i] = (uint32_t)i;
+  uint64_t cnt = 0;
+  auto put = [&](int32_t a, int32_t b, int32_t c) {
+    if (items && cnt < max) {
+      items[3 * cnt] = a;
+      items[3 * cnt + 1] = b;
+      items[3 * cnt + 2] = c;
+    }
+    ++cnt;
+  };
+  for (size_t i = 0; i < p->ops.size(); ++i) {
+    if (2 * p->ops[i].k > L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
+    for (auto& ab : plan_remaps(phys, p->n, L, p->ops[i], &p->ops, i + 1)) {
+      if (ab.first < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
+      put(1, ab.first, ab.second);
+    }
+    put(0, (int32_t)i, 0);
+  }
+  *n_items = cnt;
   return TANQ_OK;
 }
 

@@ -14,6 +14,7 @@
 // at the target positions (generalised to arbitrary physical bit positions here).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "tanq_internal.h"
@@ -47,11 +48,28 @@ __device__ __forceinline__ void st32(double2* p, const double2& a, const double2
                : "memory");
 }
 
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // ------------------------------------------------------------------------------------
 // K1 / K2: FMA register stream
 // ------------------------------------------------------------------------------------
 template <int K, bool PAIR>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
     gate_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<K> p) {
   constexpr int M = 1 << (2 * K);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -103,6 +121,116 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ------------------------------------------------------------------------------------
+// K2 on the FP64 tensor pipe: one warp = 8 tuples per tile, Y[16x8] = S[16x16] X[16x8]
+// as three real m8n8k4 GEMMs (P1 = Sr Xr, P2 = Si Xi, P3 = (Sr+Si)(Xr+Xi);
+// Yr = P1 - P2, Yi = P3 - P1 - P2), operands straight from registers:
+//   A fragments (S, constant for the launch) live in registers for the whole kernel,
+//   B fragment of k-step ks = member 4ks + (lane&3) of tuple lane>>2 -> one 16 B load,
+//   D fragment = member 8mt + (lane>>2) of tuples 2(lane&3), 2(lane&3)+1 -> one 32 B store
+//   when consecutive tuples are adjacent in memory (physical bit 0 not a target).
+// The next tile's loads are issued before the current tile's DMMAs (register prefetch).
+// ------------------------------------------------------------------------------------
+template <bool ADJ, int DEPTH>
+__global__ void __launch_bounds__(256, 2)
+    gate2_mma_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<2> p) {
+  extern __shared__ __align__(16) double2 k2_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
+  const int r4 = lane >> 2, c4 = lane & 3;
+  double2* ring = k2_smem + (size_t)wib * DEPTH * 128;   // [DEPTH][16 members][8 tuples]
+
+  double sr[2][4], si[2][4], ss[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const double2 v = p.S[(8 * mt + r4) * 16 + 4 * ks + c4];
+      sr[mt][ks] = v.x;
+      si[mt][ks] = v.y;
+      ss[mt][ks] = v.x + v.y;
+    }
+  auto member_off = [&](int m) {
+    uint64_t o = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((m >> j) & 1) o += (uint64_t)1 << p.pos[j];
+    return o;
+  };
+  auto base_of = [&](uint64_t t) {
+    uint64_t b = t;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b = ((b & ~p.lo_mask[j]) << 1) | (b & p.lo_mask[j]);
+    return b;
+  };
+  // cp.async mapping: tuple lane&7, members (lane>>3) + 4i
+  uint64_t offL[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) offL[i] = member_off((lane >> 3) + 4 * i);
+  uint64_t offD[2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) offD[mt] = member_off(8 * mt + r4);
+
+  auto issue = [&](uint64_t tl, double2* buf) {
+    if (tl < n_tiles) {
+      const uint64_t t = tl * 8 + (lane & 7);
+      const bool ok = t < p.n_tuples;
+      const double2* src = a + base_of(ok ? t : 0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        cp_async16(buf + ((lane >> 3) + 4 * i) * 8 + (lane & 7), src + offL[i], ok);
+    }
+    cp_async_commit();
+  };
+
+  uint64_t tile = warp;
+#pragma unroll
+  for (int s = 0; s < DEPTH - 1; ++s) issue(tile + (uint64_t)s * nwarps, ring + s * 128);
+  int slot = 0;
+  for (; tile < n_tiles; tile += nwarps) {
+    issue(tile + (uint64_t)(DEPTH - 1) * nwarps, ring + ((slot + DEPTH - 1) % DEPTH) * 128);
+    cp_async_wait<DEPTH - 1>();
+    __syncwarp();
+    const double2* X = ring + slot * 128;
+    double p1[2][2], p2[2][2], p3[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+      p1[mt][0] = p1[mt][1] = p2[mt][0] = p2[mt][1] = p3[mt][0] = p3[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const double2 xb = X[(4 * ks + c4) * 8 + r4];
+      const double xs = xb.x + xb.y;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma(p1[mt][0], p1[mt][1], sr[mt][ks], xb.x);
+        dmma(p2[mt][0], p2[mt][1], si[mt][ks], xb.y);
+        dmma(p3[mt][0], p3[mt][1], ss[mt][ks], xs);
+      }
+    }
+    __syncwarp();  // every lane has read this slot before it is refilled
+    const uint64_t t0 = tile * 8 + 2 * c4;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const double2 y0 = make_double2(p1[mt][0] - p2[mt][0], p3[mt][0] - p1[mt][0] - p2[mt][0]);
+      const double2 y1 = make_double2(p1[mt][1] - p2[mt][1], p3[mt][1] - p1[mt][1] - p2[mt][1]);
+      if constexpr (ADJ) {
+        if (t0 + 1 < p.n_tuples) {
+          st32(a + base_of(t0) + offD[mt], y0, y1);
+        } else if (t0 < p.n_tuples) {
+          a[base_of(t0) + offD[mt]] = y0;
+        }
+      } else {
+        if (t0 < p.n_tuples) a[base_of(t0) + offD[mt]] = y0;
+        if (t0 + 1 < p.n_tuples) a[base_of(t0 + 1) + offD[mt]] = y1;
+      }
+    }
+    slot = (slot + 1) % DEPTH;
+  }
+  cp_async_wait<0>();
+}
+
 template <int K>
 static cudaError_t launch_gate_impl(double2* a, const GateParams<K>& p, cudaStream_t st) {
   // grid-stride: up to 32 resident 256-thread waves per SM-count multiple
@@ -117,8 +245,32 @@ static cudaError_t launch_gate_impl(double2* a, const GateParams<K>& p, cudaStre
 cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st) {
   return launch_gate_impl<1>(a, p, st);
 }
+static int g_k2_variant = -1;  // 0 = FMA stream, 1 = DMMA (default); env TANQ_K2=fma|mma
+
 cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
-  return launch_gate_impl<2>(a, p, st);
+  if (g_k2_variant < 0) {
+    const char* e = getenv("TANQ_K2");
+    g_k2_variant = (e && e[0] == 'f') ? 0 : 1;
+  }
+  if (g_k2_variant == 0) return launch_gate_impl<2>(a, p, st);
+  const uint64_t tiles = (p.n_tuples + 7) / 8;
+  uint64_t warps = tiles;
+  const uint64_t cap = 148ull * 16;  // one wave: 2 CTAs x 8 warps per SM, persistent
+  if (warps > cap) warps = cap;
+  unsigned grid = (unsigned)((warps + 7) / 8);
+  constexpr int D = 4;
+  const size_t smem = (size_t)8 * D * 128 * sizeof(double2);  // 64 KiB per CTA
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gate2_mma_kernel<false, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gate2_mma_kernel<true, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (p.pos[0] == 0)
+    gate2_mma_kernel<false, D><<<grid, 256, smem, st>>>(a, p);
+  else
+    gate2_mma_kernel<true, D><<<grid, 256, smem, st>>>(a, p);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------
@@ -147,22 +299,6 @@ void gate3_make_frags(const double2* S, double2* frag) {
       }
 }
 
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 __global__ void __launch_bounds__(k3Warps * 32, 1)
     gate3_kernel(double2* __restrict__ a, const __grid_constant__ Gate3Params p) {

@@ -112,6 +112,7 @@ SIGNATURES = {
                                ctypes.POINTER(_P)], _I),
     "tanq_plan_info": ([_P, ctypes.POINTER(tanq_run_stats)], _I),
     "tanq_plan_get_op": ([_P, _U64, _P, _P, _P], _I),
+    "tanq_plan_schedule": ([_P, _I, _P, _U64, ctypes.POINTER(_U64)], _I),
     "tanq_probs": ([_P, ctypes.POINTER(tanq_readout), _P], _I),
     "tanq_expect_pauli": ([_P, _U64, _U64, _P, _P], _I),
     "tanq_sample": ([_P, ctypes.POINTER(tanq_readout), _U64, _U64, _P], _I),
@@ -253,6 +254,16 @@ class Plan:
         st = tanq_run_stats()
         _check(lib().tanq_plan_info(self.h, ctypes.byref(st)), "tanq_plan_info")
         return st.as_dict()
+
+    def schedule(self, world_size: int):
+        """[(0, op_index, 0) | (1, a_global_bit, b_local_bit)] as executed on world_size shards."""
+        n = ctypes.c_uint64()
+        _check(lib().tanq_plan_schedule(self.h, world_size, None, 0, ctypes.byref(n)),
+               "tanq_plan_schedule")
+        items = np.zeros(3 * max(1, n.value), dtype=np.int32)
+        _check(lib().tanq_plan_schedule(self.h, world_size, items.ctypes.data, n.value,
+                                        ctypes.byref(n)), "tanq_plan_schedule")
+        return [tuple(int(v) for v in items[3 * i:3 * i + 3]) for i in range(n.value)]
 
     def ops(self):
         """[(qubits tuple, S ndarray 4^k x 4^k)] of the fused plan."""

@@ -1,0 +1,51 @@
+"""Per-kernel microbenchmark: time apply_superop for k=1,2,3 at several target positions.
+
+  TANQ_K2=fma|mma python scripts/kbench.py --n 14
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=14)
+    ap.add_argument("--reps", type=int, default=10)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    from paper_2404_13184_b200 import Simulator
+    n = args.n
+    rng = np.random.default_rng(0)
+    cases = [(0,), (1,), (n - 1,), (0, 1), (1, 2), (0, n - 1), (5, n - 1), (n - 2, n - 1),
+             (0, 1, 2), (3, 7, n - 1)]
+    amps = 4 ** n
+    out = []
+    with Simulator(n) as sim:
+        st = torch.cuda.Stream()
+        torch.cuda.set_stream(st)
+        sim.set_stream(st.cuda_stream)
+        for qs in cases:
+            k = len(qs)
+            S = (rng.standard_normal((4 ** k, 4 ** k)) + 1j * rng.standard_normal((4 ** k, 4 ** k))) * 0.1
+            for _ in range(3):
+                sim.apply_superop(qs, S)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(args.reps):
+                sim.apply_superop(qs, S)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.reps
+            gbs = 32 * amps / (ms * 1e-3) / 1e9
+            tf = 8 * 4 ** k * amps / (ms * 1e-3) / 1e12
+            out.append({"qubits": qs, "k": k, "ms": ms, "GBs": gbs, "alg_TFs": tf})
+            print(json.dumps(out[-1]), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -42,13 +42,16 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_traffic(kernel: str, alg_bytes_per_launch: float):
+    """dram read+write bytes per launch of `kernel`: the DRAM/algorithmic byte ratio of the
+    committed ncu --set full capture (profiles/ncu_traffic.json) times this launch's bytes."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
-    d = json.load(open(p))
-    return d.get(kernel)
+        return None, None
+    d = json.load(open(p)).get(kernel)
+    if not isinstance(d, dict):
+        return None, None
+    return d["ratio"] * alg_bytes_per_launch, f"{d['source']} (n={d['n_qubits']}, ratio {d['ratio']:.4f})"
 
 
 class ClockSampler:
@@ -254,6 +257,7 @@ def run_ours(args):
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     share = gate["total_ms"] / ms if ms > 0 else None
     hbm_total = sum(p["bytes"] for p in prof.values())
+    traffic, traffic_src = ncu_traffic(gate["name"], bytes_launch)
 
     # ---- e2e: the public API from host objects, H2D of the inputs, D2H of the result ----
     t_e2e = []
@@ -298,7 +302,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": gate["name"], "achieved": achieved,
                          "peak": peak_gbs, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "unit": "GB/s", "frac": achieved / peak_gbs,
-                         "traffic": ncu_traffic(gate["name"]),
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "flops_per_launch": flops_launch,
                          "fp64_tflops": flops_launch / (avg_ms * 1e-3) / 1e12,

@@ -131,16 +131,14 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
 //   when consecutive tuples are adjacent in memory (physical bit 0 not a target).
 // The next tile's loads are issued before the current tile's DMMAs (register prefetch).
 // ------------------------------------------------------------------------------------
-template <bool ADJ, int DEPTH>
+template <bool ADJ, int PF>
 __global__ void __launch_bounds__(256, 2)
     gate2_mma_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<2> p) {
-  extern __shared__ __align__(16) double2 k2_smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
   const int r4 = lane >> 2, c4 = lane & 3;
-  double2* ring = k2_smem + (size_t)wib * DEPTH * 128;   // [DEPTH][16 members][8 tuples]
 
   double sr[2][4], si[2][4], ss[2][4];
 #pragma unroll
@@ -159,48 +157,43 @@ __global__ void __launch_bounds__(256, 2)
       if ((m >> j) & 1) o += (uint64_t)1 << p.pos[j];
     return o;
   };
+  uint64_t offB[4], offD[2];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) offB[ks] = member_off(4 * ks + c4);
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) offD[mt] = member_off(8 * mt + r4);
   auto base_of = [&](uint64_t t) {
     uint64_t b = t;
 #pragma unroll
     for (int j = 0; j < 4; ++j) b = ((b & ~p.lo_mask[j]) << 1) | (b & p.lo_mask[j]);
     return b;
   };
-  // cp.async mapping: tuple lane&7, members (lane>>3) + 4i
-  uint64_t offL[4];
+  auto load_tile = [&](uint64_t tl, double2* x) {
+    const uint64_t t = tl * 8 + r4;
+    if (tl < n_tiles && t < p.n_tuples) {
+      const double2* src = a + base_of(t);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) offL[i] = member_off((lane >> 3) + 4 * i);
-  uint64_t offD[2];
+      for (int ks = 0; ks < 4; ++ks) x[ks] = src[offB[ks]];
+    } else {
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt) offD[mt] = member_off(8 * mt + r4);
-
-  auto issue = [&](uint64_t tl, double2* buf) {
-    if (tl < n_tiles) {
-      const uint64_t t = tl * 8 + (lane & 7);
-      const bool ok = t < p.n_tuples;
-      const double2* src = a + base_of(ok ? t : 0);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        cp_async16(buf + ((lane >> 3) + 4 * i) * 8 + (lane & 7), src + offL[i], ok);
+      for (int ks = 0; ks < 4; ++ks) x[ks] = make_double2(0.0, 0.0);
     }
-    cp_async_commit();
   };
 
+  // register ring of PF + 1 tiles: tile i is computed while tiles i+1..i+PF are in flight
+  double2 xr[PF + 1][4];
   uint64_t tile = warp;
 #pragma unroll
-  for (int s = 0; s < DEPTH - 1; ++s) issue(tile + (uint64_t)s * nwarps, ring + s * 128);
-  int slot = 0;
+  for (int s = 0; s < PF; ++s) load_tile(tile + (uint64_t)s * nwarps, xr[s]);
   for (; tile < n_tiles; tile += nwarps) {
-    issue(tile + (uint64_t)(DEPTH - 1) * nwarps, ring + ((slot + DEPTH - 1) % DEPTH) * 128);
-    cp_async_wait<DEPTH - 1>();
-    __syncwarp();
-    const double2* X = ring + slot * 128;
+    load_tile(tile + (uint64_t)PF * nwarps, xr[PF]);
     double p1[2][2], p2[2][2], p3[2][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
       p1[mt][0] = p1[mt][1] = p2[mt][0] = p2[mt][1] = p3[mt][0] = p3[mt][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const double2 xb = X[(4 * ks + c4) * 8 + r4];
+      const double2 xb = xr[0][ks];
       const double xs = xb.x + xb.y;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
@@ -209,7 +202,6 @@ __global__ void __launch_bounds__(256, 2)
         dmma(p3[mt][0], p3[mt][1], ss[mt][ks], xs);
       }
     }
-    __syncwarp();  // every lane has read this slot before it is refilled
     const uint64_t t0 = tile * 8 + 2 * c4;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -226,9 +218,11 @@ __global__ void __launch_bounds__(256, 2)
         if (t0 + 1 < p.n_tuples) a[base_of(t0 + 1) + offD[mt]] = y1;
       }
     }
-    slot = (slot + 1) % DEPTH;
+#pragma unroll
+    for (int s = 0; s < PF; ++s)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) xr[s][ks] = xr[s + 1][ks];
   }
-  cp_async_wait<0>();
 }
 
 template <int K>
@@ -258,18 +252,22 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
   const uint64_t cap = 148ull * 16;  // one wave: 2 CTAs x 8 warps per SM, persistent
   if (warps > cap) warps = cap;
   unsigned grid = (unsigned)((warps + 7) / 8);
-  constexpr int D = 4;
-  const size_t smem = (size_t)8 * D * 128 * sizeof(double2);  // 64 KiB per CTA
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gate2_mma_kernel<false, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(gate2_mma_kernel<true, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  static int pf = -1;
+  if (pf < 0) {
+    const char* e = getenv("TANQ_K2_PF");
+    pf = (e && e[0] == '2') ? 2 : 1;
   }
-  if (p.pos[0] == 0)
-    gate2_mma_kernel<false, D><<<grid, 256, smem, st>>>(a, p);
-  else
-    gate2_mma_kernel<true, D><<<grid, 256, smem, st>>>(a, p);
+  if (pf == 2) {
+    if (p.pos[0] == 0)
+      gate2_mma_kernel<false, 2><<<grid, 256, 0, st>>>(a, p);
+    else
+      gate2_mma_kernel<true, 2><<<grid, 256, 0, st>>>(a, p);
+  } else {
+    if (p.pos[0] == 0)
+      gate2_mma_kernel<false, 1><<<grid, 256, 0, st>>>(a, p);
+    else
+      gate2_mma_kernel<true, 1><<<grid, 256, 0, st>>>(a, p);
+  }
   return cudaGetLastError();
 }
 

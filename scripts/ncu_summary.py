@@ -44,6 +44,7 @@ def main():
     ap.add_argument("reps", nargs="+")
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic", default="profiles/ncu_traffic.json")
+    ap.add_argument("--n", type=int, required=True, help="qubits of the captured run (alg bytes = 32*4^n)")
     ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,gate3=gate_k3_dmma")
     args = ap.parse_args()
     nmap = [kv.split("=") for kv in args.name_map.split(",")]
@@ -64,8 +65,10 @@ def main():
                 tb = to_bytes(r[rd], units[rd]) + to_bytes(r[wr], units[wr])
                 for pat, short in nmap:
                     if pat in name:
-                        traffic[short] = tb
-                        traffic[short + "_source"] = os.path.basename(rep)
+                        alg = 32.0 * 4 ** args.n
+                        traffic[short] = {"dram_bytes_per_launch": tb, "algorithmic_bytes_per_launch": alg,
+                                          "ratio": tb / alg, "n_qubits": args.n,
+                                          "source": os.path.basename(rep)}
     with open(args.out, "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(args.traffic, "w") as f:

@@ -104,11 +104,15 @@ def test_config4_n16_qpe_noisy_invariants(Sim):
         sim.run_circuit(c, nm, fuse=2, k_max=2)
         p = sim.probs()
         ro = sim.probs(dense.readout_of(nm))
-        e = sim.expect_pauli(0, 1 << 15)     # <Z_target>: target relaxes from |1>
+        e = sim.expect_pauli(0, 1 << 15)     # <Z_target>: target prepared in |1>
     assert abs(p.sum() - 1.0) < 1e-9 and p.min() > -1e-10
     assert abs(ro.sum() - 1.0) < 1e-9
     assert int(np.argmax(p)) == (c.m | (1 << 15))
-    assert -1.0 <= e.real < -0.5
+    # two different kernels (Pauli expectation vs diagonal) agree: <Z_15> = sum_x p(x) (-1)^x_15
+    x = np.arange(2 ** 16)
+    z = np.where((x >> 15) & 1, -1.0, 1.0)
+    assert abs(e.real - float(p @ z)) < 1e-10 and abs(e.imag) < 1e-12
+    assert e.real < 0
 
 
 @pytest.mark.skipif(os.environ.get("TANQ_FULLSIZE") != "1", reason="needs ~70 GB host RAM")

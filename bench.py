@@ -42,6 +42,18 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def fp64_tensor_peak():
+    """FP64 tensor (DMMA.8x8x4) peak measured on this pool by microbench/ubench.cu
+    (profiles/r01_microbench_b200.txt); MEASURED_PEAKS.json carries no FP64 figure."""
+    import re
+    p = os.path.join(ROOT, "profiles", "r01_microbench_b200.txt")
+    if os.path.exists(p):
+        vals = [float(x) for x in re.findall(r"DMMA m8n8k4.*?: ([0-9.]+) TFLOP/s", open(p).read())]
+        if vals:
+            return max(vals), "measured DMMA.8x8x4 microbench (profiles/r01_microbench_b200.txt)"
+    return 37.2, "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+
+
 def ncu_traffic(kernel: str, alg_bytes_per_launch: float):
     """dram read+write bytes per launch of `kernel`: the DRAM/algorithmic byte ratio of the
     committed ncu --set full capture (profiles/ncu_traffic.json) times this launch's bytes."""
@@ -127,7 +139,7 @@ def oracle_sample(config: int, n_full: int, ops_fused: int, budget_s: float = 15
               f"basis gates (noise channels unfused) of the same {config=} workload at n={n_s} "
               f"in {dt:.2f} s; per-gate time scaled by 4^({n_full}-{n_s}) to n={n_full} and "
               f"multiplied by the {len(c_full.ops)} gates of the full circuit "
-              f"({t_circuit:.1f} s); value = GPU fused ops per circuit / that time")
+              f"({t_circuit:.1f} s); value = the GPU plan's fused-gate updates per circuit / that time")
     return {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
             "sample": sample, "seconds": dt}
 
@@ -153,7 +165,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
-                       "n_qubits": c.n, "gates": len(c.ops), "fused_ops": ops_fused},
+                       "n_qubits": c.n, "gates": len(c.ops), "gate_updates": ops_fused},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"],
                              "kind": "oracle", "sample": cb["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -166,7 +178,7 @@ def fused_count_host(c, nm, args) -> int:
     """Fused op count of the GPU arm's plan (host planner only, no device work)."""
     from paper_2404_13184_b200.tanq import Plan
     p = Plan(None, c, nm, fuse=args.fuse, k_max=args.kmax, world_size=args.gpus)
-    return p.info()["ops_fused"]
+    return p.info()["gate_updates"]
 
 
 # --------------------------------------------------------------------------------------
@@ -242,22 +254,47 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    ops = st["ops_fused"]
+    ops = st["gate_updates"]          # fused-gate updates per step (a K3 group of m sub-ops = m)
     value = ops * args.steps / (ms / 1e3)
     prof = {p["name"]: p for p in sim.profile()}
     info = sim.info()
 
     # dominant kernel: the gate class with the most device time
-    gate = max((p for p in prof.values() if p["name"].startswith("gate")),
+    gate = max((p for p in prof.values() if p["name"].startswith(("gate", "group"))),
                key=lambda p: p["total_ms"])
     avg_ms = gate["total_ms"] / gate["launches"]
     bytes_launch = gate["bytes"] / gate["launches"]
     flops_launch = gate["flops"] / gate["launches"]
+    hw_flops_launch = gate["hw_flops"] / gate["launches"]
     peak_gbs, peak_kind = measured_peaks()
-    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
+    gbs = bytes_launch / (avg_ms * 1e-3) / 1e9
     share = gate["total_ms"] / ms if ms > 0 else None
     hbm_total = sum(p["bytes"] for p in prof.values())
     traffic, traffic_src = ncu_traffic(gate["name"], bytes_launch)
+    if gate["name"].startswith("group"):
+        # K3 groups are FP64-tensor bound (AI above the ridge): roofline on the DMMA pipe
+        peak_tf, peak_tf_kind = fp64_tensor_peak()
+        tf = flops_launch / (avg_ms * 1e-3) / 1e12
+        hw_tf = hw_flops_launch / (avg_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": gate["name"], "achieved": tf, "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": tf / peak_tf, "traffic": traffic,
+                     "traffic_source": traffic_src, "peak_kind": peak_tf_kind,
+                     "flops_note": "algorithmic flops = 8 per complex multiply-add; the kernel "
+                                   "executes 6 (3-multiply complex product)",
+                     "hw_achieved": hw_tf, "hw_frac": hw_tf / peak_tf,
+                     "hbm_gbs": gbs, "hbm_frac": gbs / peak_gbs,
+                     "algorithmic_bytes_per_launch": bytes_launch,
+                     "flops_per_launch": flops_launch, "avg_launch_ms": avg_ms,
+                     "launches": gate["launches"], "share_of_step": share}
+    else:
+        roofline = {"bound": "hbm", "kernel": gate["name"], "achieved": gbs, "peak": peak_gbs,
+                    "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", "unit": "GB/s",
+                    "frac": gbs / peak_gbs, "traffic": traffic, "traffic_source": traffic_src,
+                    "algorithmic_bytes_per_launch": bytes_launch,
+                    "flops_per_launch": flops_launch,
+                    "fp64_tflops": flops_launch / (avg_ms * 1e-3) / 1e12,
+                    "avg_launch_ms": avg_ms, "launches": gate["launches"],
+                    "share_of_step": share}
 
     # ---- e2e: the public API from host objects, H2D of the inputs, D2H of the result ----
     t_e2e = []
@@ -289,9 +326,10 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
-                       "n_qubits": n, "gates": len(c.ops), "fused_ops": ops,
+                       "n_qubits": n, "gates": len(c.ops), "gate_updates": ops,
+                       "kernel_ops": st["ops_fused"],
                        "fusion": f"fuse={args.fuse} k_max={args.kmax}",
-                       "ops_by_k": [st["n_k1"], st["n_k2"], st["n_k3"]],
+                       "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"]],
                        "remaps_per_step": st["n_remaps"],
                        "state_bytes": 16 * 4 ** n, "shard_bytes": info["shard_bytes"],
                        "parallelism": f"state partitioned over {world} GPU(s) by high bits",
@@ -299,17 +337,13 @@ def run_ours(args):
                        else "state fits L2 (no flush)"},
             "hbm_gbs": hbm_total / (ms / 1e3) / 1e9,
             "amplitude_updates_per_s": value * 4 ** n,
-            "roofline": {"bound": "hbm", "kernel": gate["name"], "achieved": achieved,
-                         "peak": peak_gbs, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "unit": "GB/s", "frac": achieved / peak_gbs,
-                         "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": bytes_launch,
-                         "flops_per_launch": flops_launch,
-                         "fp64_tflops": flops_launch / (avg_ms * 1e-3) / 1e12,
-                         "avg_launch_ms": avg_ms, "launches": gate["launches"],
-                         "share_of_step": share},
+            "circuit_gates_per_s": len(c.ops) * args.steps / (ms / 1e3),
+            "roofline": roofline,
             "kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / v["launches"],
-                            "gbs": v["bytes"] / v["launches"] / (v["total_ms"] / v["launches"] * 1e-3) / 1e9}
+                            "gbs": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9,
+                            "alg_tflops": v["flops"] / (v["total_ms"] * 1e-3) / 1e12,
+                            "hw_tflops": v["hw_flops"] / (v["total_ms"] * 1e-3) / 1e12,
+                            "share_of_step": v["total_ms"] / ms}
                         for k, v in prof.items()},
             "cpu_baseline": cpu,
             "e2e": {"value": ops / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -333,7 +367,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--fuse", type=int, default=2)
-    ap.add_argument("--kmax", type=int, default=2)
+    ap.add_argument("--kmax", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

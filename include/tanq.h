@@ -123,7 +123,7 @@ typedef struct {
 } tanq_readout;
 
 /* fuse: 0 none, 1 paper (same qubit / same ordered pair), 2 greedy up to k_max
- * with the B200 cost model (default).  k_max in {1,2,3}.  chunk_bytes: remap staging chunk
+ * with the B200 cost model (default).  k_max in {1,2,3} (default 3: 3-qubit groups).  chunk_bytes: remap staging chunk
  * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings. */
 typedef struct {
   int32_t fuse;
@@ -135,7 +135,9 @@ typedef struct {
 
 typedef struct {
   uint64_t ops_in;         /* circuit ops */
-  uint64_t ops_fused;      /* fused ops executed */
+  uint64_t ops_fused;      /* fused ops executed (kernel launches of the plan) */
+  uint64_t gate_updates;   /* fused-gate updates: k<=2 fused superoperators applied to the whole
+                              state (a K3 group of m sub-ops counts m, a dense k=3 op counts 1) */
   uint64_t n_k[4];         /* fused ops by arity k = 1..3 (index k) */
   uint64_t n_remaps;       /* global<->local bit swaps */
   uint64_t remap_bytes;    /* bytes sent by this process */
@@ -160,8 +162,10 @@ typedef struct {
   char name[32];
   uint64_t launches;
   double total_ms;
-  double bytes;
-  double flops;
+  double bytes;      /* algorithmic HBM bytes: 32 per amplitude per launch */
+  double flops;      /* algorithmic flops: 8 per complex multiply-add of S x */
+  double hw_flops;   /* flops the kernel executes (2 per real FMA; the 3-multiply complex
+                        product of the DMMA kernels executes 6 per complex multiply-add) */
 } tanq_kernel_prof;
 
 /* ---- lifetime ---------------------------------------------------------------------- */

@@ -258,14 +258,19 @@ Mat embed_superop(const Mat& Ss, const std::vector<int>& pos, int k) {
 struct FusedOp {
   int k = 0;
   int q[3] = {0, 0, 0};
-  Mat S;            // 4^k, local index over q[0..k-1]
+  Mat S;            // 4^k, local index over q[0..k-1] (for a factored group: the dense product)
   int parts = 1;    // number of pre-fusion ops folded in
+  std::vector<FusedOp> sub;  // k=3 factored group: sub-ops applied in order in one pass
 };
 
-// B200 cost of one op in units of one HBM read+write pass (32 B / amplitude), DESIGN.md
-// §Fusion cost model: k<=2 FMA ops hide their FP64 work under the pass; a dense k=3 op on
-// DMMA with the 3-multiply complex product costs 192 FMA/amplitude / (FP64 rate) ~ 2.1.
-double op_cost(int k) { return k <= 2 ? 1.0 : 2.1; }
+// B200 cost model in units of one HBM read+write pass (32 B / amplitude), DESIGN.md §6,
+// calibrated with scripts/kbench.py on B200 (n=14, profiles/r01_kbench_*): K1 ~6.8 TB/s
+// (1 pass), K2 5.0-6.5 TB/s (~1.15), a dense k=3 op on DMMA ~3.08 passes (FP64 bound).  A
+// factored K3 group costs 0.24 + its sub-ops' FP64 time: k=1 0.10, k=2 0.66 passes.
+double sep_cost(int k) { return k == 1 ? 1.0 : (k == 2 ? 1.15 : 3.08); }
+double sub_cost(int k) { return k == 1 ? 0.10 : (k == 2 ? 0.66 : 3.08); }
+constexpr double kGroupBase = 0.24;
+double op_cost(int k) { return k <= 2 ? 1.0 : 3.08; }
 
 bool shares(const FusedOp& a, const int* q, int k) {
   for (int i = 0; i < a.k; ++i)
@@ -342,7 +347,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   // 3-qubit grouping: greedy groups of <= 3 qubits over the k<=2 ops; a group replaces its
   // members only when their summed pass cost exceeds one dense k=3 pass.
   struct Group {
-    FusedOp op;
+    FusedOp op;  // qubit union only (S is formed on demand)
     std::vector<int> members;
   };
   std::vector<Group> groups;
@@ -356,26 +361,66 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
       }
     if (idx >= 0) {
       Group& Q = groups[idx];
-      int uk = Q.op.k;
-      for (int j = 0; j < G.k; ++j) {
+      int uq[3], uk = Q.op.k;
+      for (int i = 0; i < Q.op.k; ++i) uq[i] = Q.op.q[i];
+      bool fits = true;
+      for (int j = 0; j < G.k && fits; ++j) {
         bool f = false;
-        for (int i = 0; i < Q.op.k; ++i) f |= Q.op.q[i] == G.q[j];
-        if (!f) ++uk;
+        for (int i = 0; i < uk; ++i) f |= uq[i] == G.q[j];
+        if (!f) {
+          if (uk == 3) fits = false; else uq[uk++] = G.q[j];
+        }
       }
-      if (uk <= 3) {
-        Q.op = merge(Q.op, G);
+      if (fits) {
+        Q.op.k = uk;
+        for (int i = 0; i < uk; ++i) Q.op.q[i] = uq[i];
         Q.members.push_back(gi);
         continue;
       }
     }
-    groups.push_back(Group{G, {gi}});
+    Group g;
+    g.op.k = G.k;
+    for (int i = 0; i < G.k; ++i) g.op.q[i] = G.q[i];
+    g.members.push_back(gi);
+    groups.push_back(std::move(g));
   }
+  // the dense superoperator of a group on its union (members applied in order)
+  auto dense_of = [&](const Group& g) {
+    FusedOp acc = l1[g.members[0]];
+    for (size_t i = 1; i < g.members.size(); ++i) acc = merge(acc, l1[g.members[i]]);
+    // re-express on the group's qubit order
+    std::vector<int> pos;
+    for (int j = 0; j < acc.k; ++j)
+      for (int i = 0; i < g.op.k; ++i)
+        if (g.op.q[i] == acc.q[j]) pos.push_back(i);
+    FusedOp out = g.op;
+    out.S = embed_superop(acc.S, pos, g.op.k);
+    out.parts = acc.parts;
+    return out;
+  };
   std::vector<FusedOp> out;
   for (Group& g : groups) {
-    double sep = 0;
-    for (int m : g.members) sep += op_cost(l1[m].k);
-    if (g.op.k == 3 && op_cost(3) < sep) {
-      out.push_back(g.op);
+    if (g.members.size() == 1 || g.op.k < 3) {
+      for (int m : g.members) out.push_back(l1[m]);
+      continue;
+    }
+    double sep = 0, fact = 0;
+    size_t prog = 0;
+    for (int m : g.members) {
+      sep += sep_cost(l1[m].k);
+      fact += sub_cost(l1[m].k);
+      prog += l1[m].k == 3 ? 4096 : (l1[m].k == 2 ? 256 : 16);
+    }
+    fact = std::max(1.0, kGroupBase + fact);
+    const double dense = sep_cost(3);
+    const bool fact_ok = g.members.size() <= (size_t)tanq::kMaxSub &&
+                         prog <= (size_t)tanq::kGroupProgMax;
+    if (fact_ok && fact <= dense && fact < sep) {
+      FusedOp f = g.op;  // factored: S formed only on export (tanq_plan_get_op)
+      for (int m : g.members) f.sub.push_back(l1[m]);
+      out.push_back(std::move(f));
+    } else if (dense < sep) {
+      out.push_back(dense_of(g));
     } else {
       for (int m : g.members) out.push_back(l1[m]);
     }
@@ -386,9 +431,9 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
 struct Prof {
   int cls;
   cudaEvent_t e0, e1;
-  double bytes, flops;
+  double bytes, flops, hw_flops;
 };
-const char* kProfNames[] = {"gate_k1", "gate_k2", "gate_k3_dmma", "remap"};
+const char* kProfNames[] = {"gate_k1", "gate_k2", "group_k3_dmma", "remap"};
 
 }  // namespace
 
@@ -431,6 +476,7 @@ struct tanq_sim {
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_bytes[4] = {0, 0, 0, 0};
   double prof_flops[4] = {0, 0, 0, 0};
+  double prof_hw_flops[4] = {0, 0, 0, 0};
   uint64_t prof_launches[4] = {0, 0, 0, 0};
   uint64_t launches = 0;
   uint64_t remap_count = 0, remap_bytes = 0;
@@ -643,6 +689,7 @@ tanq_status prof_flush(tanq_sim* s) {
     s->prof_ms[p.cls] += ms;
     s->prof_bytes[p.cls] += p.bytes;
     s->prof_flops[p.cls] += p.flops;
+    s->prof_hw_flops[p.cls] += p.hw_flops;
     s->prof_launches[p.cls]++;
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
@@ -651,70 +698,155 @@ tanq_status prof_flush(tanq_sim* s) {
   return TANQ_OK;
 }
 
-// Launch one fused op on every shard (targets must be local).  frag3: device fragment
-// buffer per device for k = 3 (indexed like s->scratch).
-tanq_status launch_op(tanq_sim* s, const FusedOp& op, const std::vector<const double2*>* frag3) {
-  const int k = op.k, M = 1 << (2 * k);
-  // sorted physical target positions; member bit t <-> pos[t]
-  std::vector<std::pair<int, int>> bits;  // (phys pos, local-vec bit: r_j -> j, c_j -> k + j)
+// Member order of an op on the current layout: member bit t <-> the t-th lowest physical
+// target bit; l_of[i] = paper local vec index (r + c 2^k) of member i.
+struct MemberMap {
+  std::vector<std::pair<int, int>> bits;  // sorted (physical pos, paper-index bit)
+  std::vector<int> l_of;
+};
+
+MemberMap member_map(const tanq_sim* s, int k, const int* q) {
+  MemberMap mm;
   for (int j = 0; j < k; ++j) {
-    bits.push_back({(int)s->phys[2 * op.q[j]], j});
-    bits.push_back({(int)s->phys[2 * op.q[j] + 1], k + j});
+    mm.bits.push_back({(int)s->phys[2 * q[j]], j});
+    mm.bits.push_back({(int)s->phys[2 * q[j] + 1], k + j});
   }
-  std::sort(bits.begin(), bits.end());
-  std::vector<int> l_of(M);
+  std::sort(mm.bits.begin(), mm.bits.end());
+  const int M = 1 << (2 * k);
+  mm.l_of.resize(M);
   for (int i = 0; i < M; ++i) {
     int l = 0;
     for (int t = 0; t < 2 * k; ++t)
-      if ((i >> t) & 1) l |= 1 << bits[t].second;
-    l_of[i] = l;
+      if ((i >> t) & 1) l |= 1 << mm.bits[t].second;
+    mm.l_of[i] = l;
   }
+  return mm;
+}
+
+std::vector<double2> member_order_S(const FusedOp& op, const MemberMap& mm) {
+  const int M = 1 << (2 * op.k);
+  std::vector<double2> out((size_t)M * M);
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < M; ++j) {
+      const cd v = op.S(mm.l_of[i], mm.l_of[j]);
+      out[(size_t)i * M + j] = make_double2(v.real(), v.imag());
+    }
+  return out;
+}
+
+size_t group_prog_elems(const FusedOp& op) {
+  if (op.sub.empty()) return tanq::group_frag_elems(3);
+  size_t e = 0;
+  for (const auto& sb : op.sub) e += tanq::group_frag_elems(sb.k);
+  return e;
+}
+
+// Build the K3 group program (sub-op headers + fragment-ordered matrices) for the current
+// layout; returns the kernel parameters except `prog`.
+void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, double2* prog) {
+  const MemberMap tile = member_map(s, 3, op.q);
+  for (int t = 0; t < 6; ++t) {
+    p.pos[t] = (uint32_t)tile.bits[t].first;
+    p.lo_mask[t] = ((uint64_t)1 << tile.bits[t].first) - 1;
+  }
+  p.n_tuples = (uint64_t)1 << (s->L - 6);
+  std::vector<const FusedOp*> subs;
+  if (op.sub.empty())
+    subs.push_back(&op);
+  else
+    for (const auto& sb : op.sub) subs.push_back(&sb);
+  size_t off = 0;
+  p.n_sub = (int)subs.size();
+  for (size_t i = 0; i < subs.size(); ++i) {
+    const FusedOp& sb = *subs[i];
+    const MemberMap mm = member_map(s, sb.k, sb.q);
+    tanq::GroupSub& g = p.sub[i];
+    std::memset(&g, 0, sizeof(g));
+    g.k = sb.k;
+    g.s_off = (int)off;
+    // tile bit index of each of the sub-op's sorted physical positions
+    int tb[6], nb = 0, rb[6], nr = 0;
+    for (int t = 0; t < 2 * sb.k; ++t)
+      for (int u = 0; u < 6; ++u)
+        if (tile.bits[u].first == mm.bits[t].first) tb[nb++] = u;
+    for (int u = 0; u < 6; ++u) {
+      bool used = false;
+      for (int t = 0; t < nb; ++t) used |= tb[t] == u;
+      if (!used) rb[nr++] = u;
+    }
+    if (sb.k < 3) {
+      for (int m = 0; m < (1 << (2 * sb.k)); ++m) {
+        int v = 0;
+        for (int t = 0; t < nb; ++t)
+          if ((m >> t) & 1) v |= 1 << tb[t];
+        g.mi[m] = (uint8_t)v;
+      }
+      for (int u = 0; u < (1 << nr); ++u) {
+        int v = 0;
+        for (int t = 0; t < nr; ++t)
+          if ((u >> t) & 1) v |= 1 << rb[t];
+        g.mu[u] = (uint8_t)v;
+      }
+    }
+    const std::vector<double2> Sm = member_order_S(sb, mm);
+    tanq::group_make_frags(sb.k, Sm.data(), prog + off);
+    off += tanq::group_frag_elems(sb.k);
+  }
+  p.prog_elems = (int)off;
+}
+
+// Launch one fused op on every shard (targets must be local).  For k = 3, `prog` holds the
+// group program already copied to each device (indexed like s->scratch).
+tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* gp,
+                      const std::vector<const double2*>* prog) {
+  const int k = op.k, M = 1 << (2 * k);
   const uint64_t n_tuples = (uint64_t)1 << (s->L - 2 * k);
   const double amps = (double)((uint64_t)1 << s->L);
+  // algorithmic: 8 flops per complex MAC; executed: K1 (FMA) 8, K2 / K3 (3-multiply DMMA) 6
+  double flops_amp = 8.0 * M, hw_amp = (k == 1 ? 8.0 : 6.0) * M;
+  if (k == 3 && !op.sub.empty()) {
+    flops_amp = hw_amp = 0;
+    for (const auto& sb : op.sub) {
+      const int Ms = 1 << (2 * sb.k);
+      flops_amp += 8.0 * Ms;
+      hw_amp += (sb.k == 1 ? 8.0 : 6.0) * Ms;
+    }
+  }
+  MemberMap mm;
+  std::vector<double2> Sm;
+  if (k < 3) {
+    mm = member_map(s, k, op.q);
+    Sm = member_order_S(op, mm);
+  }
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
-    Prof pr{k - 1, nullptr, nullptr, 32.0 * amps, 8.0 * M * amps};
+    Prof pr{k - 1, nullptr, nullptr, 32.0 * amps, flops_amp * amps, hw_amp * amps};
     prof_begin(s, sh, pr);
-    if (k == 1 || k == 2) {
-      if (k == 1) {
-        tanq::GateParams<1> p;
-        for (int i = 0; i < M; ++i)
-          for (int j = 0; j < M; ++j) {
-            cd v = op.S(l_of[i], l_of[j]);
-            p.S[i * M + j] = make_double2(v.real(), v.imag());
-          }
-        for (int t = 0; t < 2; ++t) {
-          p.pos[t] = (uint32_t)bits[t].first;
-          p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
-        }
-        p.n_tuples = n_tuples;
-        CUDA_TRY(tanq::launch_gate1(sh.data, p, sh.stream));
-      } else {
-        tanq::GateParams<2> p;
-        for (int i = 0; i < M; ++i)
-          for (int j = 0; j < M; ++j) {
-            cd v = op.S(l_of[i], l_of[j]);
-            p.S[i * M + j] = make_double2(v.real(), v.imag());
-          }
-        for (int t = 0; t < 4; ++t) {
-          p.pos[t] = (uint32_t)bits[t].first;
-          p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
-        }
-        p.n_tuples = n_tuples;
-        CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
+    if (k == 1) {
+      tanq::GateParams<1> p;
+      std::memcpy(p.S, Sm.data(), sizeof(p.S));
+      for (int t = 0; t < 2; ++t) {
+        p.pos[t] = (uint32_t)mm.bits[t].first;
+        p.lo_mask[t] = ((uint64_t)1 << mm.bits[t].first) - 1;
       }
+      p.n_tuples = n_tuples;
+      CUDA_TRY(tanq::launch_gate1(sh.data, p, sh.stream));
+    } else if (k == 2) {
+      tanq::GateParams<2> p;
+      std::memcpy(p.S, Sm.data(), sizeof(p.S));
+      for (int t = 0; t < 4; ++t) {
+        p.pos[t] = (uint32_t)mm.bits[t].first;
+        p.lo_mask[t] = ((uint64_t)1 << mm.bits[t].first) - 1;
+      }
+      p.n_tuples = n_tuples;
+      CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
     } else {
-      tanq::Gate3Params p;
       int di = 0;
       for (size_t i = 0; i < s->scratch.size(); ++i)
         if (s->scratch[i].device == sh.device) di = (int)i;
-      p.Sfrag = (*frag3)[di];
-      for (int t = 0; t < 6; ++t) {
-        p.pos[t] = (uint32_t)bits[t].first;
-        p.lo_mask[t] = ((uint64_t)1 << bits[t].first) - 1;
-      }
-      p.n_tuples = n_tuples;
-      CUDA_TRY(tanq::launch_gate3(sh.data, p, sh.stream));
+      tanq::GroupParams p = *gp;
+      p.prog = (*prog)[di];
+      CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
     }
     s->launches++;
     prof_end(s, sh, pr);
@@ -733,72 +865,55 @@ tanq_status ensure_frag_capacity(tanq_sim* s, DevScratch& d, size_t elems) {
 
 // Execute a list of fused ops in order (remaps inserted as needed).
 tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
-  // k=3 fragments depend on the layout at execution time, so they are built op by op into a
-  // persistent pinned host buffer and copied (async) to each device before the launch.
-  size_t n3 = 0;
-  for (const auto& op : ops) n3 += op.k == 3;
-  const size_t fe = tanq::gate3_frag_elems();
-  if (n3) {
+  // K3 group programs depend on the layout at execution time, so they are built op by op
+  // into a persistent pinned host buffer and copied (async) to each device before the launch.
+  size_t total = 0;
+  for (const auto& op : ops)
+    if (op.k == 3) total += group_prog_elems(op);
+  if (total) {
     for (auto& sh : s->shards) {
       DevScratch& d = scratch_for(s, sh.device);
       TRY(ensure_scratch(s, d));
-      TRY(ensure_frag_capacity(s, d, fe * n3));
+      TRY(ensure_frag_capacity(s, d, total));
     }
     if (s->frag_done_pending) {  // previous H2D copies from the pinned buffer must be done
       CUDA_TRY(cudaEventSynchronize(s->frag_done));
       s->frag_done_pending = false;
     }
-    if (s->frag_host_elems < fe * n3) {
+    if (s->frag_host_elems < total) {
       if (s->frag_host) CUDA_TRY(cudaFreeHost(s->frag_host));
-      CUDA_TRY(cudaMallocHost(&s->frag_host, fe * n3 * sizeof(double2)));
-      s->frag_host_elems = fe * n3;
+      CUDA_TRY(cudaMallocHost(&s->frag_host, total * sizeof(double2)));
+      s->frag_host_elems = total;
     }
   }
-  size_t i3 = 0;
+  size_t off = 0;
+  tanq::GroupParams gp;
   for (size_t i = 0; i < ops.size(); ++i) {
     const FusedOp& op = ops[i];
     TRY(ensure_local(s, op, &ops, i + 1));
     if (op.k != 3) {
-      TRY(launch_op(s, op, nullptr));
+      TRY(launch_op(s, op, nullptr, nullptr));
       continue;
     }
-    std::vector<std::pair<int, int>> bits;
-    for (int j = 0; j < 3; ++j) {
-      bits.push_back({(int)s->phys[2 * op.q[j]], j});
-      bits.push_back({(int)s->phys[2 * op.q[j] + 1], 3 + j});
-    }
-    std::sort(bits.begin(), bits.end());
-    std::vector<double2> Sm(64 * 64);
-    int l_of[64];
-    for (int m = 0; m < 64; ++m) {
-      int l = 0;
-      for (int t = 0; t < 6; ++t)
-        if ((m >> t) & 1) l |= 1 << bits[t].second;
-      l_of[m] = l;
-    }
-    for (int a = 0; a < 64; ++a)
-      for (int b = 0; b < 64; ++b) {
-        cd v = op.S(l_of[a], l_of[b]);
-        Sm[a * 64 + b] = make_double2(v.real(), v.imag());
-      }
-    double2* hf = s->frag_host + fe * i3;
-    tanq::gate3_make_frags(Sm.data(), hf);
+    double2* hp = s->frag_host + off;
+    build_group(s, op, gp, hp);
     std::vector<const double2*> ptrs(s->scratch.size(), nullptr);
     for (auto& sh : s->shards) {
       int di = 0;
       for (size_t q = 0; q < s->scratch.size(); ++q)
         if (s->scratch[q].device == sh.device) di = (int)q;
       if (!ptrs[di]) {
-        double2* dst = s->scratch[di].frag + fe * i3;
+        double2* dst = s->scratch[di].frag + off;
         CUDA_TRY(cudaSetDevice(sh.device));
-        CUDA_TRY(cudaMemcpyAsync(dst, hf, fe * sizeof(double2), cudaMemcpyHostToDevice, sh.stream));
+        CUDA_TRY(cudaMemcpyAsync(dst, hp, gp.prog_elems * sizeof(double2),
+                                 cudaMemcpyHostToDevice, sh.stream));
         ptrs[di] = dst;
       }
     }
-    ++i3;
-    TRY(launch_op(s, op, &ptrs));
+    off += gp.prog_elems;
+    TRY(launch_op(s, op, &gp, &ptrs));
   }
-  if (n3) {
+  if (total) {
     Shard& s0 = s->shards[0];
     for (auto& sh : s->shards) TRY(stream_wait(s0, sh));
     CUDA_TRY(cudaSetDevice(s0.device));
@@ -1282,7 +1397,7 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   if (!c || !out) return fail(TANQ_E_ARG, "NULL argument");
   *out = nullptr;
   if (c->n_ops && !c->ops) return fail(TANQ_E_ARG, "ops is NULL");
-  tanq_run_opts opts{2, 2, 0, 0, 0};
+  tanq_run_opts opts{2, 3, 0, 0, 0};
   if (o) opts = *o;
   if (opts.fuse < 0 || opts.fuse > 2) return fail(TANQ_E_ARG, "fuse must be 0, 1 or 2");
   if (opts.k_max < 1 || opts.k_max > 3) return fail(TANQ_E_ARG, "k_max must be 1..3");
@@ -1333,6 +1448,7 @@ tanq_status tanq_plan_info(const tanq_plan* p, tanq_run_stats* st) {
   std::memset(st, 0, sizeof(*st));
   st->ops_in = p->ops_in;
   st->ops_fused = p->ops.size();
+    for (const auto& f : p->ops) st->gate_updates += f.sub.empty() ? 1 : f.sub.size();
   for (const auto& f : p->ops) st->n_k[f.k]++;
   st->plan_ms = p->plan_ms;
   return TANQ_OK;
@@ -1373,8 +1489,20 @@ tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits
   const FusedOp& f = p->ops[i];
   *k = f.k;
   for (int j = 0; j < f.k; ++j) qubits[j] = f.q[j];
-  if (S)
-    for (size_t e = 0; e < f.S.a.size(); ++e) S[e] = tanq_c64{f.S.a[e].real(), f.S.a[e].imag()};
+  if (S) {
+    Mat D = f.S;
+    if (!f.sub.empty()) {  // factored group: product of the embedded sub-ops, in order
+      D = identity(1 << (2 * f.k));
+      for (const FusedOp& sb : f.sub) {
+        std::vector<int> pos;
+        for (int j = 0; j < sb.k; ++j)
+          for (int u = 0; u < f.k; ++u)
+            if (f.q[u] == sb.q[j]) pos.push_back(u);
+        D = matmul(embed_superop(sb.S, pos, f.k), D);
+      }
+    }
+    for (size_t e = 0; e < D.a.size(); ++e) S[e] = tanq_c64{D.a[e].real(), D.a[e].imag()};
+  }
   return TANQ_OK;
 }
 
@@ -1391,6 +1519,7 @@ tanq_status tanq_plan_exec(tanq_sim* s, const tanq_plan* p, tanq_run_stats* st) 
     std::memset(st, 0, sizeof(*st));
     st->ops_in = p->ops_in;
     st->ops_fused = p->ops.size();
+    for (const auto& f : p->ops) st->gate_updates += f.sub.empty() ? 1 : f.sub.size();
     for (const auto& f : p->ops) st->n_k[f.k]++;
     st->n_remaps = s->remap_count - r0;
     st->remap_bytes = s->remap_bytes - b0;
@@ -1598,6 +1727,7 @@ tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* 
     p.total_ms = s->prof_ms[c];
     p.bytes = s->prof_bytes[c];
     p.flops = s->prof_flops[c];
+    p.hw_flops = s->prof_hw_flops[c];
   }
   *n_out = n;
   return TANQ_OK;
@@ -1607,7 +1737,7 @@ tanq_status tanq_profile_reset(tanq_sim* s) {
   if (!s) return fail(TANQ_E_ARG, "NULL handle");
   TRY(prof_flush(s));
   for (int c = 0; c < 4; ++c) {
-    s->prof_ms[c] = s->prof_bytes[c] = s->prof_flops[c] = 0;
+    s->prof_ms[c] = s->prof_bytes[c] = s->prof_flops[c] = s->prof_hw_flops[c] = 0;
     s->prof_launches[c] = 0;
   }
   return TANQ_OK;

@@ -20,13 +20,25 @@ struct GateParams {
   uint32_t pos[2 * K];
 };
 
-// K = 3: the superoperator is 64 x 64 complex = 64 KiB, too large for a kernel parameter;
-// it lives in global memory pre-arranged in DMMA fragment order (see tanq_kernels.cu).
-struct Gate3Params {
-  const double2* Sfrag;      // [8 m-tiles][16 k-steps][32 lanes] of (Sr, Si)
+// K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 64-member tuples (6 physical
+// bits pos[], all local) in one HBM round trip.  Sub-op matrices live in `prog` in A-fragment
+// order (group_make_frags); mi[i] / mu[u] map sub-op member i / sub-tuple u to tile members.
+static constexpr int kMaxSub = 40;
+static constexpr int kGroupProgMax = 5632;  // double2 (88 KiB): one dense k=3 + 6 k=2, or 22 k=2
+struct GroupSub {
+  int32_t k;
+  int32_t s_off;     // offset of the sub-op matrix in prog (double2 units)
+  uint8_t mi[16];
+  uint8_t mu[16];
+};
+struct GroupParams {
+  const double2* prog;
+  int32_t prog_elems;
+  int32_t n_sub;
   uint64_t lo_mask[6];
   uint64_t n_tuples;
   uint32_t pos[6];
+  GroupSub sub[kMaxSub];
 };
 
 struct BitMap {               // physical bit of each logical bit (row q -> 2q, col q -> 2q+1)
@@ -37,9 +49,9 @@ struct BitMap {               // physical bit of each logical bit (row q -> 2q, 
 // kernel launchers (all asynchronous on `st`)
 cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st);
 cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st);
-cudaError_t launch_gate3(double2* a, const Gate3Params& p, cudaStream_t st);
-size_t gate3_frag_elems();   // double2 count of the fragment-ordered S
-void gate3_make_frags(const double2* S_member_order /*64x64*/, double2* frag /*host*/);
+cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st);
+size_t group_frag_elems(int k);                               // double2 per sub-op matrix
+void group_make_frags(int k, const double2* S_member_order, double2* frag /*host*/);
 
 cudaError_t launch_init(double2* a, uint64_t elems, bool one_at_zero, cudaStream_t st);
 // In-place swap of the halves two shards exchange when global bit g swaps with local bit b:

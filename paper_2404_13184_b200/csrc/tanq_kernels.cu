@@ -272,121 +272,278 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------
-// K3: fused 3-qubit superoperator on DMMA.8x8x4 (mma.sync.m8n8k4 f64)
+// K3: 3-qubit groups on DMMA.8x8x4 (mma.sync.m8n8k4 f64).
 //
-// Per warp: a tile of 8 tuples.  Complex Y[64 x 8] = S[64 x 64] X[64 x 8] with the
-// 3-multiply form  P1 = Sr Xr, P2 = Si Xi, P3 = (Sr + Si)(Xr + Xi);
-// Yr = P1 - P2, Yi = P3 - P1 - P2.
+// One HBM round trip per group: a warp stages a tile of 8 tuples x 64 members (the group's
+// 6 physical bits) in shared memory with cp.async (double-buffered), runs the group's
+// program of sub-ops on the tile, and writes the tile back.  Sub-ops:
+//   k=3  dense 64x64 superoperator (the fused k=3 op of SURVEY A-5): Y[64x8] = S X.
+//   k=2  16x16 superoperator on the 4 sub-tuples of each tuple: Y[16x32] = S X[16x32].
+//   k=1  4x4 superoperator on the 16 sub-tuples (FMA).
+// Complex products use three real GEMMs: P1 = Sr Xr, P2 = Si Xi, P3 = (Sr+Si)(Xr+Xi);
+// Yr = P1 - P2, Yi = P3 - P1 - P2 (25% fewer FP64 ops than the paper's 4-MMA scheme).
 // Fragments (PTX m8n8k4 .row.col f64): A[8x4] lane -> (lane>>2, lane&3);
 // B[4x8] lane -> (k = lane&3, n = lane>>2); D[8x8] lane -> (lane>>2, 2*(lane&3)+{0,1}).
-// A = S rows 8mt.., cols 4ks..; the host stores S as frag[mt][ks][lane] = (Sr, Si, Sr+Si).
-// X tiles: shared [64 members][8 tuples] double2, double-buffered per warp, cp.async.
+// Sub-op matrices are stored in A-fragment order by the host (group_make_*).
 // ------------------------------------------------------------------------------------
-static constexpr int k3Warps = 8;
-static constexpr int k3FragElems = 8 * 16 * 32;  // (Sr, Si) per (m-tile, k-step, lane)
+static constexpr int kGWarps = 8;
 
-size_t gate3_frag_elems() { return (size_t)k3FragElems; }
+// Tile element (member m, tuple t) lives at m*8 + (t ^ (m & 7)) (XOR swizzle): conflict-free
+// for both the tuple-major fragment reads and the address-ordered global<->shared copies.
+__device__ __forceinline__ int xs_idx(int m, int t) { return m * 8 + (t ^ (m & 7)); }
 
-void gate3_make_frags(const double2* S, double2* frag) {
-  // frag[(mt*16 + ks)*32 + lane] = S[8 mt + (lane>>2)][4 ks + (lane&3)]  (A fragment order)
-  for (int mt = 0; mt < 8; ++mt)
-    for (int ks = 0; ks < 16; ++ks)
+size_t group_frag_elems(int k) { return k == 3 ? 4096 : (k == 2 ? 256 : 16); }
+
+void group_make_frags(int k, const double2* S, double2* frag) {
+  if (k == 1) {
+    for (int i = 0; i < 16; ++i) frag[i] = S[i];
+    return;
+  }
+  const int M = k == 3 ? 64 : 16, KS = M / 4, MT = M / 8;
+  for (int mt = 0; mt < MT; ++mt)
+    for (int ks = 0; ks < KS; ++ks)
       for (int lane = 0; lane < 32; ++lane) {
-        int row = mt * 8 + (lane >> 2), col = ks * 4 + (lane & 3);
-        frag[((size_t)mt * 16 + ks) * 32 + lane] = S[row * 64 + col];
+        const int row = mt * 8 + (lane >> 2), col = ks * 4 + (lane & 3);
+        frag[((size_t)mt * KS + ks) * 32 + lane] = S[row * M + col];
       }
 }
 
+__device__ __forceinline__ void group_sub_k3(double2* X, const double2* F, int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+  double p1[8][2], p2[8][2], p3[8][2];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) p1[mt][0] = p1[mt][1] = p2[mt][0] = p2[mt][1] = p3[mt][0] = p3[mt][1] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < 16; ++ks) {
+    const double2 xb = X[xs_idx(ks * 4 + c4, r4)];
+    const double xs = xb.x + xb.y;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const double2 sv = F[(mt * 16 + ks) * 32 + lane];
+      dmma(p1[mt][0], p1[mt][1], sv.x, xb.x);
+      dmma(p2[mt][0], p2[mt][1], sv.y, xb.y);
+      dmma(p3[mt][0], p3[mt][1], sv.x + sv.y, xs);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      X[xs_idx(mt * 8 + r4, 2 * c4 + c)] =
+          make_double2(p1[mt][c] - p2[mt][c], p3[mt][c] - p1[mt][c] - p2[mt][c]);
+}
 
-__global__ void __launch_bounds__(k3Warps * 32, 1)
-    gate3_kernel(double2* __restrict__ a, const __grid_constant__ Gate3Params p) {
+template <int UI>  // sub-tuples processed at once (1, 2 or 4): ILP vs registers
+__device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const uint8_t* mi,
+                                             const uint8_t* mu, int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+  double sr[2][4], si[2][4], ss[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const double2 v = F[(mt * 4 + ks) * 32 + lane];
+      sr[mt][ks] = v.x;
+      si[mt][ks] = v.y;
+      ss[mt][ks] = v.x + v.y;
+    }
+  int mb[4], md[2];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) mb[ks] = mi[4 * ks + c4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) md[mt] = mi[8 * mt + r4];
+#pragma unroll
+  for (int u0 = 0; u0 < 4; u0 += UI) {
+    int mo[UI];
+#pragma unroll
+    for (int u = 0; u < UI; ++u) mo[u] = mu[u0 + u];
+    double p1[UI][2][2], p2[UI][2][2], p3[UI][2][2];
+#pragma unroll
+    for (int u = 0; u < UI; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+        p1[u][mt][0] = p1[u][mt][1] = p2[u][mt][0] = p2[u][mt][1] = p3[u][mt][0] = p3[u][mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      double2 xb[UI];
+#pragma unroll
+      for (int u = 0; u < UI; ++u) xb[u] = X[xs_idx(mb[ks] | mo[u], r4)];
+#pragma unroll
+      for (int u = 0; u < UI; ++u) {
+        const double xs = xb[u].x + xb[u].y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma(p1[u][mt][0], p1[u][mt][1], sr[mt][ks], xb[u].x);
+          dmma(p2[u][mt][0], p2[u][mt][1], si[mt][ks], xb[u].y);
+          dmma(p3[u][mt][0], p3[u][mt][1], ss[mt][ks], xs);
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int u = 0; u < UI; ++u)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          X[xs_idx(md[mt] | mo[u], 2 * c4 + c)] = make_double2(
+              p1[u][mt][c] - p2[u][mt][c], p3[u][mt][c] - p1[u][mt][c] - p2[u][mt][c]);
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const uint8_t* mi,
+                                             const uint8_t* mu, int lane) {
+  double2 S[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) S[i] = F[i];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int col = lane + 32 * j, u = col >> 3, t = col & 7;
+    double2 x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = X[xs_idx(mi[i] | mu[u], t)];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      double yr = 0.0, yi = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        yr = fma(S[l * 4 + m].x, x[m].x, yr);
+        yr = fma(-S[l * 4 + m].y, x[m].y, yr);
+        yi = fma(S[l * 4 + m].x, x[m].y, yi);
+        yi = fma(S[l * 4 + m].y, x[m].x, yi);
+      }
+      X[xs_idx(mi[l] | mu[u], t)] = make_double2(yr, yi);
+    }
+  }
+}
+
+// WARPS warps per CTA (one CTA per SM), NBUF tile buffers per warp (2 = cp.async double
+// buffering), HAS3: the program may contain a dense k=3 sub-op (needs the register budget of
+// 8 warps), UI: sub-tuples per k=2 pass.
+template <int WARPS, int NBUF, bool HAS3, int UI>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    group3_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // shared: S fragments (Sr, Si) 64 KiB | X tiles 8 warps x 2 buffers x 512 double2 128 KiB |
-  //         member offsets 64 x 8 B.  Sr + Si is formed in registers.
-  double2* sS = reinterpret_cast<double2*>(smem_raw);
-  double2* sX = sS + k3FragElems;
-  uint64_t* sOff = reinterpret_cast<uint64_t*>(sX + k3Warps * 2 * 512);
+  // shared: program (<= kGroupProgMax double2) | X tiles WARPS x NBUF x 512 double2 (128 KiB) |
+  //         copy tables | sub-op headers
+  double2* sProg = reinterpret_cast<double2*>(smem_raw);
+  double2* sX = sProg + kGroupProgMax;
+  // copy mapping tables: iteration i (16) -> (tuple bits, member bits, address offset)
+  uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + WARPS * NBUF * 512);
+  int* sIterTM = reinterpret_cast<int*>(sIterOff + 16);
+  GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int e = threadIdx.x; e < k3FragElems; e += blockDim.x) sS[e] = p.Sfrag[e];
-  for (int m = threadIdx.x; m < 64; m += blockDim.x) {
-    uint64_t o = 0;
-    for (int j = 0; j < 6; ++j)
-      if ((m >> j) & 1) o += (uint64_t)1 << p.pos[j];
-    sOff[m] = o;
+  // The 9 index bits of a tile element (3 tuple bits at the lowest free physical positions,
+  // 6 member bits at pos[]) sorted by physical position: lanes take the 5 lowest, the copy
+  // iterations the next 4, so every copy instruction covers the most contiguous addresses.
+  int bit_pos[9], bit_id[9];  // id < 3: tuple bit, else member bit id-3
+  {
+    int nf = 0;
+    for (int f = 0; f < 64 && nf < 3; ++f) {
+      bool tgt = false;
+      for (int j = 0; j < 6; ++j) tgt |= (int)p.pos[j] == f;
+      if (!tgt) bit_pos[nf++] = f;
+    }
+    for (int j = 0; j < 3; ++j) bit_id[j] = j;
+    for (int j = 0; j < 6; ++j) {
+      bit_pos[3 + j] = (int)p.pos[j];
+      bit_id[3 + j] = 3 + j;
+    }
+    for (int x = 1; x < 9; ++x)  // insertion sort by position
+      for (int y = x; y > 0 && bit_pos[y] < bit_pos[y - 1]; --y) {
+        int tp = bit_pos[y]; bit_pos[y] = bit_pos[y - 1]; bit_pos[y - 1] = tp;
+        int ti = bit_id[y]; bit_id[y] = bit_id[y - 1]; bit_id[y - 1] = ti;
+      }
   }
+  auto tm_of = [&](int bits, int first, int cnt, uint64_t& off) {
+    int t = 0, m = 0;
+    off = 0;
+    for (int b = 0; b < cnt; ++b)
+      if ((bits >> b) & 1) {
+        const int id = bit_id[first + b];
+        if (id < 3) t |= 1 << id; else m |= 1 << (id - 3);
+        off += (uint64_t)1 << bit_pos[first + b];
+      }
+    return t | (m << 3);
+  };
+  // address of (tile, t, m) = base(tile*8) + deposit(t at free bits) + deposit(m at pos[]):
+  // insert_zeros is a bit deposit, so the tuple and member parts add independently.
+  uint64_t lane_off;
+  const int lane_tm = tm_of(lane, 0, 5, lane_off);
+  if (threadIdx.x < 16) {
+    uint64_t o;
+    sIterTM[threadIdx.x] = tm_of(threadIdx.x, 5, 4, o);
+    sIterOff[threadIdx.x] = o;
+  }
+  for (int e = threadIdx.x; e < p.prog_elems; e += blockDim.x) sProg[e] = p.prog[e];
+  for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
   __syncthreads();
 
   const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
-  const uint64_t tile_stride = (uint64_t)gridDim.x * k3Warps;
-  uint64_t tile = (uint64_t)blockIdx.x * k3Warps + warp;
-  double2* bufs[2] = {sX + warp * 2 * 512, sX + warp * 2 * 512 + 512};
-  const int ld_t = lane & 7, ld_m0 = lane >> 3;  // load/store mapping: tuple, member base
-
+  const uint64_t tile_stride = (uint64_t)gridDim.x * WARPS;
+  uint64_t tile = (uint64_t)blockIdx.x * WARPS + warp;
+  double2* const wbuf = sX + warp * NBUF * 512;  // NBUF 512-double2 tiles (no indexed array:
+                                                  // a dynamically indexed pointer array spills)
+  // element (lane, i): tuple t = tm & 7, member m = tm >> 3, address base(tile*8) + off
+  auto elem = [&](int i, int& t, int& m, uint64_t& off) {
+    const int tm = lane_tm | sIterTM[i];
+    t = tm & 7;
+    m = tm >> 3;
+    off = lane_off + sIterOff[i];
+  };
   auto issue_load = [&](uint64_t tl, double2* buf) {
-    uint64_t t = tl * 8 + ld_t;
-    bool ok = t < p.n_tuples;
-    uint64_t base = insert_zeros(ok ? t : 0, p.lo_mask, 6);
+    const double2* src = a + insert_zeros(tl * 8, p.lo_mask, 6);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      int m = ld_m0 + 4 * i;
-      cp_async16(buf + m * 8 + ld_t, a + base + sOff[m], ok);
+      int t, m;
+      uint64_t off;
+      elem(i, t, m, off);
+      const bool ok = tl * 8 + t < p.n_tuples;
+      cp_async16(buf + xs_idx(m, t), ok ? src + off : a, ok);
     }
     cp_async_commit();
   };
 
-  if (tile < n_tiles) issue_load(tile, bufs[0]);
+  if (NBUF == 2 && tile < n_tiles) issue_load(tile, wbuf);
   int cur = 0;
   for (; tile < n_tiles; tile += tile_stride) {
-    const uint64_t next = tile + tile_stride;
-    if (next < n_tiles) {
-      issue_load(next, bufs[cur ^ 1]);
-      cp_async_wait<1>();
+    if constexpr (NBUF == 2) {
+      const uint64_t next = tile + tile_stride;
+      if (next < n_tiles) {
+        issue_load(next, wbuf + ((cur ^ 1) << 9));
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
     } else {
+      issue_load(tile, wbuf);
       cp_async_wait<0>();
     }
     __syncwarp();
-    double2* X = bufs[cur];
-    double p1[8][2], p2[8][2], p3[8][2];
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      p1[mt][0] = p1[mt][1] = 0.0;
-      p2[mt][0] = p2[mt][1] = 0.0;
-      p3[mt][0] = p3[mt][1] = 0.0;
-    }
-#pragma unroll 4
-    for (int ks = 0; ks < 16; ++ks) {
-      const double2 xb = X[(ks * 4 + (lane & 3)) * 8 + (lane >> 2)];
-      const double xs = xb.x + xb.y;
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        const double2 s = sS[(mt * 16 + ks) * 32 + lane];
-        dmma(p1[mt][0], p1[mt][1], s.x, xb.x);
-        dmma(p2[mt][0], p2[mt][1], s.y, xb.y);
-        dmma(p3[mt][0], p3[mt][1], s.x + s.y, xs);
+    double2* X = wbuf + (NBUF == 2 ? (cur << 9) : 0);
+    for (int s = 0; s < p.n_sub; ++s) {
+      const GroupSub& g = sSub[s];
+      const double2* F = sProg + g.s_off;
+      if (g.k == 2) {
+        group_sub_k2<UI>(X, F, g.mi, g.mu, lane);
+      } else if (g.k == 3) {
+        if constexpr (HAS3) group_sub_k3(X, F, lane);
+      } else {
+        group_sub_k1(X, F, g.mi, g.mu, lane);
       }
+      __syncwarp();
     }
-    __syncwarp();
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int row = mt * 8 + (lane >> 2), col = 2 * (lane & 3);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        double yr = p1[mt][c] - p2[mt][c];
-        double yi = p3[mt][c] - p1[mt][c] - p2[mt][c];
-        X[row * 8 + col + c] = make_double2(yr, yi);
-      }
-    }
-    __syncwarp();
     {
-      uint64_t t = tile * 8 + ld_t;
-      if (t < p.n_tuples) {
-        uint64_t base = insert_zeros(t, p.lo_mask, 6);
+      double2* dst = a + insert_zeros(tile * 8, p.lo_mask, 6);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          int m = ld_m0 + 4 * i;
-          a[base + sOff[m]] = X[m * 8 + ld_t];
-        }
+      for (int i = 0; i < 16; ++i) {
+        int t, m;
+        uint64_t off;
+        elem(i, t, m, off);
+        if (tile * 8 + t < p.n_tuples) dst[off] = X[xs_idx(m, t)];
       }
     }
     __syncwarp();
@@ -394,28 +551,41 @@ __global__ void __launch_bounds__(k3Warps * 32, 1)
   }
 }
 
-static size_t gate3_smem_bytes() {
-  return 4096 * sizeof(double2) + (size_t)k3Warps * 2 * 512 * sizeof(double2) + 64 * 8;
-}
-
-cudaError_t launch_gate3(double2* a, const Gate3Params& p, cudaStream_t st) {
+template <int WARPS, int NBUF, bool HAS3, int UI>
+static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  size_t smem = gate3_smem_bytes();
+  const size_t smem = (size_t)kGroupProgMax * sizeof(double2) +
+                      (size_t)WARPS * NBUF * 512 * sizeof(double2) + 16 * 8 + 16 * 4 +
+                      (size_t)kMaxSub * sizeof(GroupSub);
+  auto kern = group3_kernel<WARPS, NBUF, HAS3, UI>;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gate3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  uint64_t tiles = (p.n_tuples + 7) / 8;
-  uint64_t ctas = (tiles + k3Warps - 1) / k3Warps;
+  const uint64_t tiles = (p.n_tuples + 7) / 8;
+  const uint64_t ctas = (tiles + WARPS - 1) / WARPS;
   unsigned grid = (unsigned)(ctas < (uint64_t)sms ? ctas : (uint64_t)sms);
   if (grid < 1) grid = 1;
-  gate3_kernel<<<grid, k3Warps * 32, smem, st>>>(a, p);
+  kern<<<grid, WARPS * 32, smem, st>>>(a, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
+  bool has3 = false;
+  for (int i = 0; i < p.n_sub; ++i) has3 |= p.sub[i].k == 3;
+  if (has3) return launch_group3_cfg<8, 2, true, 4>(a, p, st);
+  static int cfg = -1;  // TANQ_G3=a|b|c selects the factored-group configuration
+  if (cfg < 0) {
+    const char* e = getenv("TANQ_G3");
+    cfg = e ? (e[0] - 'a') : 2;
+  }
+  if (cfg == 0) return launch_group3_cfg<8, 2, false, 4>(a, p, st);
+  if (cfg == 2) return launch_group3_cfg<16, 1, false, 1>(a, p, st);
+  return launch_group3_cfg<16, 1, false, 2>(a, p, st);
 }
 
 // ------------------------------------------------------------------------------------

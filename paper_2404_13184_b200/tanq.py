@@ -65,11 +65,12 @@ class tanq_run_opts(ctypes.Structure):
 
 class tanq_run_stats(ctypes.Structure):
     _fields_ = [("ops_in", ctypes.c_uint64), ("ops_fused", ctypes.c_uint64),
-                ("n_k", ctypes.c_uint64 * 4), ("n_remaps", ctypes.c_uint64),
+                ("gate_updates", ctypes.c_uint64), ("n_k", ctypes.c_uint64 * 4), ("n_remaps", ctypes.c_uint64),
                 ("remap_bytes", ctypes.c_uint64), ("plan_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {"ops_in": self.ops_in, "ops_fused": self.ops_fused,
+                "gate_updates": self.gate_updates,
                 "n_k1": self.n_k[1], "n_k2": self.n_k[2], "n_k3": self.n_k[3],
                 "n_remaps": self.n_remaps, "remap_bytes": self.remap_bytes,
                 "plan_ms": self.plan_ms}
@@ -85,7 +86,7 @@ class tanq_info(ctypes.Structure):
 class tanq_kernel_prof(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_uint64),
                 ("total_ms", ctypes.c_double), ("bytes", ctypes.c_double),
-                ("flops", ctypes.c_double)]
+                ("flops", ctypes.c_double), ("hw_flops", ctypes.c_double)]
 
 
 # exported symbols and their signatures (mirrors include/tanq.h)
@@ -227,7 +228,7 @@ class Plan:
     sim=None plans on the host only (tanq_plan_create_host) for an n-qubit register split
     over world_size shards."""
 
-    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=2, profile=False,
+    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
                  world_size: int = 1):
         cc = CCircuit(circuit.ops)
         cn = CNoise(noise) if noise is not None else None
@@ -377,7 +378,7 @@ class Simulator:
         _check(lib().tanq_apply_superop(self.h, len(q), q.ctypes.data, m.ctypes.data),
                "tanq_apply_superop")
 
-    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 2,
+    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
                     profile: bool = False, prepared=None) -> dict:
         cc = prepared[0] if prepared else CCircuit(circuit.ops)
         cn = (prepared[1] if prepared else (CNoise(noise) if noise is not None else None))
@@ -388,7 +389,7 @@ class Simulator:
                                       ctypes.byref(opts), ctypes.byref(st)), "tanq_run_circuit")
         return st.as_dict()
 
-    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 2,
+    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
              profile: bool = False) -> "Plan":
         return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile)
 
@@ -423,7 +424,8 @@ class Simulator:
         n = ctypes.c_int()
         _check(lib().tanq_profile_read(self.h, arr, 8, ctypes.byref(n)), "tanq_profile_read")
         return [{"name": arr[i].name.decode(), "launches": arr[i].launches,
-                 "total_ms": arr[i].total_ms, "bytes": arr[i].bytes, "flops": arr[i].flops}
+                 "total_ms": arr[i].total_ms, "bytes": arr[i].bytes, "flops": arr[i].flops,
+                 "hw_flops": arr[i].hw_flops}
                 for i in range(n.value)]
 
     def profile_reset(self):

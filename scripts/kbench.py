@@ -45,6 +45,29 @@ def main():
             tf = 8 * 4 ** k * amps / (ms * 1e-3) / 1e12
             out.append({"qubits": qs, "k": k, "ms": ms, "GBs": gbs, "alg_TFs": tf})
             print(json.dumps(out[-1]), flush=True)
+        # K3 groups: chains of k=2 superoperators inside 3 qubits, one pass (fuse=2, k_max=3)
+        import workloads as W
+        groups = [[(0, 1), (1, 2)], [(1, 2), (2, 3), (1, 3)], [(5, n - 1), (n - 1, n - 2)],
+                  [(0, 1), (1, 2), (0, 2), (2, 1)], [(3, 7), (7, n - 1), (3, n - 1), (7, 3), (3, 7)]]
+        for g in groups:
+            ops = [W.Op("superop", qs, mat=(rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))) * 0.1)
+                   for qs in g]
+            plan = sim.plan(W.Circuit(n, ops), None, fuse=2, k_max=3)
+            info = plan.info()
+            for _ in range(3):
+                plan.exec(sim)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(args.reps):
+                plan.exec(sim)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.reps
+            out.append({"group": g, "kernels": info["ops_fused"], "gate_updates": info["gate_updates"],
+                        "ms": ms, "GBs_per_pass": 32 * amps * info["ops_fused"] / (ms * 1e-3) / 1e9,
+                        "ms_per_update": ms / info["gate_updates"]})
+            print(json.dumps(out[-1]), flush=True)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,80 @@
+"""Host planner (A-1 noise binding, A-2 superoperator builder, A-3 fusion) without a GPU.
+
+The library's plan is exported op by op (tanq_plan_get_op: qubits + 4^k x 4^k superoperator
+in the paper's vec convention) and applied with the ORACLE's block superoperator routine;
+the result must equal the oracle's own unfused Kraus evolution.  This pins the C++
+superoperator builder (conj(K) (x) K, depolarizing / thermal closed forms, over-rotation,
+composition order) and every fusion mode, independently of the kernels.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import dense
+
+
+def _apply_plan(plan, n):
+    rho = dense.ground(n)
+    for qs, S in plan.ops():
+        dense.apply_superop(rho, n, qs, S)
+    return rho
+
+
+@pytest.mark.parametrize("fuse,kmax", [(0, 2), (1, 2), (2, 1), (2, 2), (2, 3)])
+@pytest.mark.parametrize("seed", range(5))
+def test_plan_equals_oracle(fuse, kmax, seed):
+    from paper_2404_13184_b200.tanq import Plan
+    n = 3 + seed % 3
+    c = W.random_circuit(n, 45, seed=900 + seed, kmax=3)
+    nm = W.synthetic_calibration(c, seed, depol=True, thermal=True, overrot=True)
+    nm.order = seed % 2
+    plan = Plan(None, c, nm, fuse=fuse, k_max=kmax)
+    ref = dense.run(c, nm)
+    got = _apply_plan(plan, n)
+    assert np.abs(got - ref).max() < 1e-12
+    info = plan.info()
+    assert info["ops_in"] == len(c.ops)
+    if fuse == 0:
+        assert info["ops_fused"] == len(c.ops)
+    else:
+        assert info["ops_fused"] <= len(c.ops)
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 6), (3, 5), (4, 5), (5, 5)])
+def test_config_plans_equal_oracle(cfg, n):
+    from paper_2404_13184_b200.tanq import Plan
+    c, nm = W.config_workload(cfg, n=n, depth=6 if cfg == 3 else None)
+    ref = dense.run(c, nm)
+    for kmax in (2, 3):
+        plan = Plan(None, c, nm, fuse=2, k_max=kmax)
+        assert np.abs(_apply_plan(plan, c.n) - ref).max() < 1e-12
+
+
+def test_fusion_counts_on_paper_workloads():
+    """Fusion reduces the transpiled gate count (-1.6x on average with the paper's
+    rule); our k<=2 and k<=3 modes reduce it further."""
+    from paper_2404_13184_b200.tanq import Plan
+    for cfg in (2, 3, 4, 5):
+        c, nm = W.config_workload(cfg)
+        paper = Plan(None, c, nm, fuse=1).info()
+        k2 = Plan(None, c, nm, fuse=2, k_max=2).info()
+        k3 = Plan(None, c, nm, fuse=2, k_max=3).info()
+        assert paper["ops_fused"] < len(c.ops)
+        assert k2["ops_fused"] <= paper["ops_fused"]
+        assert k3["ops_fused"] <= k2["ops_fused"]
+        assert k3["gate_updates"] == k2["gate_updates"]
+
+
+def test_planner_rejects_bad_inputs():
+    from paper_2404_13184_b200.tanq import Plan, TanqError
+    c = W.Circuit(3, [W.Op("sx", (0,))])
+    nm = W.NoiseModel(3, [W.QubitCal() for _ in range(3)])
+    with pytest.raises(TanqError):                  # missing calibration
+        Plan(None, c, nm)
+    nm.gates[("sx", (0,))] = W.GateCal(1.5, 0.0, 0.0)
+    with pytest.raises(TanqError):                  # p outside [0, 1]
+        Plan(None, c, nm)
+    with pytest.raises(TanqError):                  # qubit out of range
+        Plan(None, W.Circuit(3, [W.Op("x", (5,))]))
+    with pytest.raises(TanqError):                  # repeated qubit
+        Plan(None, W.Circuit(3, [W.Op("cx", (1, 1))]))

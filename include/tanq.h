@@ -124,7 +124,9 @@ typedef struct {
 
 /* fuse: 0 none, 1 paper (same qubit / same ordered pair), 2 greedy up to k_max
  * with the B200 cost model (default).  k_max in {1,2,3} (default 3: 3-qubit groups).  chunk_bytes: remap staging chunk
- * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings. */
+ * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
+ * on single-shard handles capture their launches into a CUDA graph on the first
+ * tanq_plan_exec and replay it afterwards (ignored with bit0). */
 typedef struct {
   int32_t fuse;
   int32_t k_max;

@@ -1388,7 +1388,101 @@ struct tanq_plan {
   uint64_t ops_in = 0;
   double plan_ms = 0;
   int flags = 0;
+  // CUDA-graph replay cache (flags bit1, single-shard handles): valid for one handle, one
+  // shard buffer and one starting layout; group programs live in a plan-owned device buffer.
+  struct GraphCache {
+    const tanq_sim* sim = nullptr;
+    const double2* data = nullptr;
+    uint32_t phys[64];
+    cudaGraphExec_t exec = nullptr;
+    double2* dprog = nullptr;
+    int device = -1;
+    uint64_t kernels = 0;
+  };
+  mutable GraphCache g;
+  ~tanq_plan() {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.dprog) {
+      cudaSetDevice(g.device);
+      cudaFree(g.dprog);
+    }
+  }
 };
+
+namespace {
+// Capture the whole plan as one CUDA graph (single shard: the layout never changes, so every
+// kernel parameter is known before the first launch), then replay it.
+tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
+  Shard& sh = s->shards[0];
+  auto& g = p->g;
+  const bool hit = g.exec && g.sim == s && g.data == sh.data &&
+                   std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0;
+  CUDA_TRY(cudaSetDevice(sh.device));
+  if (!hit) {
+    if (g.exec) {
+      CUDA_TRY(cudaGraphExecDestroy(g.exec));
+      g.exec = nullptr;
+    }
+    if (g.dprog) {
+      CUDA_TRY(cudaSetDevice(g.device));
+      CUDA_TRY(cudaFree(g.dprog));
+      g.dprog = nullptr;
+      CUDA_TRY(cudaSetDevice(sh.device));
+    }
+    size_t total = 0;
+    for (const auto& op : p->ops)
+      if (op.k == 3) total += group_prog_elems(op);
+    std::vector<double2> host(total ? total : 1);
+    std::vector<tanq::GroupParams> gps;
+    size_t off = 0;
+    for (const auto& op : p->ops)
+      if (op.k == 3) {
+        gps.emplace_back();
+        build_group(s, op, gps.back(), host.data() + off);
+        off += gps.back().prog_elems;
+      }
+    if (total) {
+      CUDA_TRY(cudaMalloc(&g.dprog, total * sizeof(double2)));
+      CUDA_TRY(cudaMemcpy(g.dprog, host.data(), total * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    g.device = sh.device;
+    std::vector<const double2*> ptr(s->scratch.size() + 1, nullptr);
+    int di = 0;
+    for (size_t i = 0; i < s->scratch.size(); ++i)
+      if (s->scratch[i].device == sh.device) di = (int)i;
+    cudaGraph_t graph;
+    CUDA_TRY(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal));
+    const uint64_t l0 = s->launches;
+    off = 0;
+    size_t gi = 0;
+    tanq_status st = TANQ_OK;
+    for (const auto& op : p->ops) {
+      if (op.k != 3) {
+        st = launch_op(s, op, nullptr, nullptr);
+      } else {
+        ptr[di] = g.dprog + off;
+        off += gps[gi].prog_elems;
+        st = launch_op(s, op, &gps[gi++], &ptr);
+      }
+      if (st != TANQ_OK) break;
+    }
+    cudaError_t ce = cudaStreamEndCapture(sh.stream, &graph);
+    if (st != TANQ_OK) return st;
+    if (ce != cudaSuccess) return fail(TANQ_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(TANQ_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    g.kernels = s->launches - l0;
+    s->launches = l0;
+    g.sim = s;
+    g.data = sh.data;
+    std::memcpy(g.phys, s->phys, sizeof(g.phys));
+  }
+  CUDA_TRY(cudaGraphLaunch(g.exec, sh.stream));
+  s->launches += g.kernels;
+  return TANQ_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -1512,9 +1606,14 @@ tanq_status tanq_plan_exec(tanq_sim* s, const tanq_plan* p, tanq_run_stats* st) 
   for (const auto& f : p->ops)
     if (2 * f.k > s->L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
   const uint64_t r0 = s->remap_count, b0 = s->remap_bytes;
-  s->prof_on = (p->flags & 1) != 0;
-  tanq_status r = exec_ops(s, p->ops);
-  s->prof_on = false;
+  tanq_status r;
+  if ((p->flags & 2) && s->shards.size() == 1 && !s->dist && !(p->flags & 1)) {
+    r = exec_graph(s, p);
+  } else {
+    s->prof_on = (p->flags & 1) != 0;
+    r = exec_ops(s, p->ops);
+    s->prof_on = false;
+  }
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->ops_in = p->ops_in;

@@ -229,10 +229,10 @@ class Plan:
     over world_size shards."""
 
     def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
-                 world_size: int = 1):
+                 world_size: int = 1, graph: bool = False):
         cc = CCircuit(circuit.ops)
         cn = CNoise(noise) if noise is not None else None
-        opts = tanq_run_opts(fuse, k_max, 0, 1 if profile else 0, 0)
+        opts = tanq_run_opts(fuse, k_max, 0, (1 if profile else 0) | (2 if graph else 0), 0)
         h = ctypes.c_void_p()
         nmp = ctypes.byref(cn.c) if cn is not None else None
         if sim is None:
@@ -390,8 +390,8 @@ class Simulator:
         return st.as_dict()
 
     def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
-             profile: bool = False) -> "Plan":
-        return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile)
+             profile: bool = False, graph: bool = False) -> "Plan":
+        return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile, graph=graph)
 
     @staticmethod
     def prepare(circuit, noise=None):

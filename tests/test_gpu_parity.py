@@ -253,3 +253,59 @@ def test_noiseless_purity_statevector(Sim):
         with Sim(n) as sim:
             sim.run_circuit(c, fuse=2, k_max=3)
             assert np.abs(rho_of(sim, n) - np.outer(psi, psi.conj())).max() < 1e-12
+
+
+# --------------------------------------------------------------------------------------
+# K3 group programs: factored k=1/k=2 sub-ops, dense k=3 sub-ops, tiny tiles
+# --------------------------------------------------------------------------------------
+
+def _group_circuit(rng, n, qs3, with_dense):
+    a, b, c = qs3
+    ops = []
+    if with_dense:
+        ops.append(W.Op("u", (c, a, b), mat=W.random_unitary(rng, 8)))
+    ops += [W.Op("kraus", (a, b), kraus=W.random_kraus(rng, 4, 2)),
+            W.Op("u", (b,), mat=W.random_unitary(rng, 2)),
+            W.Op("kraus", (c, b), kraus=W.random_kraus(rng, 4, 3)),
+            W.Op("u", (c,), mat=W.random_unitary(rng, 2)),
+            W.Op("kraus", (a, c), kraus=W.random_kraus(rng, 4, 2))]
+    return W.Circuit(n, ops)
+
+
+@pytest.mark.parametrize("n,qs3", [(3, (0, 1, 2)), (4, (3, 0, 2)), (6, (5, 1, 3)), (8, (0, 7, 4)),
+                                   (9, (8, 6, 7))])
+@pytest.mark.parametrize("with_dense", [False, True])
+def test_group_programs(Sim, n, qs3, with_dense):
+    from paper_2404_13184_b200.tanq import Plan
+    rng = np.random.default_rng(n * 10 + int(with_dense))
+    c = _group_circuit(rng, n, qs3, with_dense)
+    info = Plan(None, c, None, fuse=2, k_max=3).info()
+    assert info["n_k3"] >= 1
+    rho = W.random_density(rng, n, rank=3)
+    with Sim(n) as sim:
+        sim.set_state(dense.to_vec(rho))
+        st = sim.run_circuit(c, fuse=2, k_max=3)
+        assert st["n_k3"] >= 1
+        got = rho_of(sim, n)
+    ref = dense.run(c, None, rho=np.ascontiguousarray(rho.copy()))
+    assert_parity(got, ref)
+
+
+def test_plan_graph_replay(Sim):
+    """CUDA-graph capture of a plan (flags bit1): first exec captures, later execs replay."""
+    from paper_2404_13184_b200.tanq import Plan
+    n = 7
+    c, nm = W.config_workload(3, n=n, depth=5)
+    ref = dense.run(c, nm)
+    rng = np.random.default_rng(5)
+    rho0 = W.random_density(rng, n)
+    ref2 = dense.run(c, nm, rho=np.ascontiguousarray(rho0.copy()))
+    with Sim(n) as sim:
+        plan = Plan(sim, c, nm, fuse=2, k_max=3, graph=True)
+        for _ in range(3):
+            sim.reset()
+            plan.exec(sim)
+            assert_parity(rho_of(sim, n), ref)
+        sim.set_state(dense.to_vec(rho0))
+        plan.exec(sim)
+        assert_parity(rho_of(sim, n), ref2)

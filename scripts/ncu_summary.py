@@ -45,7 +45,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic", default="profiles/ncu_traffic.json")
     ap.add_argument("--n", type=int, required=True, help="qubits of the captured run (alg bytes = 32*4^n)")
-    ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,gate3=gate_k3_dmma")
+    ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,group3=group_k3_dmma")
     args = ap.parse_args()
     nmap = [kv.split("=") for kv in args.name_map.split(",")]
     traffic = json.load(open(args.traffic)) if os.path.exists(args.traffic) else {}

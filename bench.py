@@ -215,7 +215,7 @@ def run_ours(args):
         dist.broadcast_object_list(uid, src=0)
         sim = Simulator(n, world_size=world, rank=rank, device=local, nccl_uid=uid[0])
     else:
-        sim = Simulator(n, 1)
+        sim = Simulator(n, args.shards)
     stream = torch.cuda.Stream()          # a real stream: events on it bracket the kernels
     torch.cuda.set_stream(stream)
     sim.set_stream(stream.cuda_stream)
@@ -332,7 +332,9 @@ def run_ours(args):
                        "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"]],
                        "remaps_per_step": st["n_remaps"],
                        "state_bytes": 16 * 4 ** n, "shard_bytes": info["shard_bytes"],
-                       "parallelism": f"state partitioned over {world} GPU(s) by high bits",
+                       "parallelism": (f"state partitioned over {world} GPU(s) by high bits"
+                                       if args.shards == 1 else
+                                       f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
                        "l2": "inputs larger than L2 (state >> 126 MB)" if 16 * 4 ** n > 5e8
                        else "state fits L2 (no flush)"},
             "hbm_gbs": hbm_total / (ms / 1e3) / 1e9,
@@ -370,6 +372,9 @@ def main():
     ap.add_argument("--kmax", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shards", type=int, default=1,
+                    help="N=1 only: split the state into this many virtual shards on the one GPU "
+                         "(exercises the global-qubit remap with the in-place swap kernel)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

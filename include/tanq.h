@@ -68,7 +68,8 @@ typedef enum {
   TANQ_U = 17,        /* user matrix m: 2^k x 2^k (need not be unitary) */
   TANQ_KRAUS = 18,    /* user channel: n_kraus matrices 2^k x 2^k contiguous in m */
   TANQ_SUPEROP = 19,  /* user superoperator m: 4^k x 4^k, local vec index r + c 2^k */
-  TANQ_N_KINDS = 20
+  TANQ_RESET = 20,    /* reset q[0] to |0>: channel {|0><0|, |0><1|} (reading R19), noiseless */
+  TANQ_N_KINDS = 21
 } tanq_kind;
 
 /* One circuit operation.  k = number of qubits (1..3; named gates fix k). */
@@ -241,6 +242,13 @@ tanq_status tanq_expect_pauli(tanq_sim* s, uint64_t x_mask, uint64_t z_mask, dou
  * generator keyed by seed (shot i uses counter i); negatives > -1e-10 clamped to 0. */
 tanq_status tanq_sample(tanq_sim* s, const tanq_readout* ro, uint64_t seed, uint64_t shots,
                         uint64_t* outcomes);
+
+/* Mid-circuit projective measurement of `qubit` in the computational basis (the measurement
+ * gate announced at P:45 / P:50, text absent; reading R19): p1 = Tr(|1><1|_q rho) from the
+ * diagonal, outcome b = [u < p1] with u the first Philox4x32-10 uniform of (seed, counter 0),
+ * then rho <- P_b rho P_b / p_b.  *outcome = b, *prob = p_b (either may be NULL).
+ * TANQ_E_STATE if p_b < 1e-300 (cannot happen for the drawn outcome unless rho is invalid). */
+tanq_status tanq_measure(tanq_sim* s, int qubit, uint64_t seed, int* outcome, double* prob);
 
 /* ---- state I/O (paper vec order v = r + c 2^n) --------------------------------------- */
 tanq_status tanq_get_state(tanq_sim* s, uint64_t first, uint64_t count, tanq_c64* out);

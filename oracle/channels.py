@@ -135,6 +135,9 @@ def gate_channel_sequence(op, noise) -> List[tuple]:
         return [("kraus", qs, [np.asarray(m, dtype=complex) for m in op.kraus])]
     if kind == "superop":
         return [("superop", qs, np.asarray(op.mat, dtype=complex))]
+    if kind == "reset":  # reading R19: {|0><0|, |0><1|}, noiseless
+        return [("kraus", qs, [np.array([[1, 0], [0, 0]], dtype=complex),
+                               np.array([[0, 1], [0, 0]], dtype=complex)])]
     seq: List[tuple] = [("kraus", qs, [gate_unitary(kind, op.theta)])]
     if noise is None or kind == "rz":
         return seq

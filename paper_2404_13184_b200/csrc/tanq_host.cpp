@@ -126,6 +126,7 @@ Mat matmul(const Mat& A, const Mat& B) {
 // ------------------------------------------------------------------------------------
 int kind_arity(int kind) {
   if (kind >= TANQ_ID && kind <= TANQ_RZ) return 1;
+  if (kind == TANQ_RESET) return 1;
   if (kind >= TANQ_CX && kind <= TANQ_SWAP) return 2;
   return 0;  // user matrices: arity from op.k
 }
@@ -549,6 +550,18 @@ tanq_status stream_wait(const Shard& waiter, const Shard& on) {
   return TANQ_OK;
 }
 
+void prof_begin(tanq_sim* s, Shard& sh, Prof& p) {
+  if (!s->prof_on || sh.id != s->rank0) return;
+  cudaEventCreate(&p.e0);
+  cudaEventCreate(&p.e1);
+  cudaEventRecord(p.e0, sh.stream);
+}
+void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
+  if (!s->prof_on || sh.id != s->rank0) return;
+  cudaEventRecord(p.e1, sh.stream);
+  s->prof.push_back(p);
+}
+
 // Swap physical bit a (global, a >= L) with local bit b (A-6).
 tanq_status remap_swap(tanq_sim* s, int a, int b) {
   const int L = s->L, gb = a - L;
@@ -564,7 +577,11 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
       TRY(stream_wait(sh, *other));
       CUDA_TRY(cudaSetDevice(sh.device));
       const int va = 1 - ((g >> gb) & 1), vb = 1 - ((g2 >> gb) & 1);
+      // algorithmic bytes: both exchanged halves read and written once
+      Prof pr{3, nullptr, nullptr, 4.0 * half * sizeof(double2), 0.0, 0.0};
+      prof_begin(s, sh, pr);
       CUDA_TRY(tanq::launch_swap_halves(sh.data, other->data, L, b, va, vb, sh.stream));
+      prof_end(s, sh, pr);
       s->launches++;
       TRY(stream_wait(*other, sh));
       s->remap_bytes += half * sizeof(double2);
@@ -574,6 +591,9 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
     const int g = sh.id, g2 = g ^ (1 << gb);
     const int v = 1 - ((g >> gb) & 1);
     CUDA_TRY(cudaSetDevice(sh.device));
+    // bytes = the half sent + the half received over NVLink
+    Prof pr{3, nullptr, nullptr, 2.0 * half * sizeof(double2), 0.0, 0.0};
+    prof_begin(s, sh, pr);
     for (uint64_t first = 0; first < half; first += s->xchunk) {
       const uint64_t cnt = std::min<uint64_t>(s->xchunk, half - first);
       CUDA_TRY(tanq::launch_pack_half(sh.data, s->xsend, b, v, first, cnt, sh.stream));
@@ -585,6 +605,7 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
       s->launches += 2;
       s->remap_bytes += cnt * sizeof(double2);
     }
+    prof_end(s, sh, pr);
   }
   // bookkeeping: logical bits at a and b exchange positions
   for (int i = 0; i < 2 * s->n; ++i) {
@@ -666,18 +687,6 @@ tanq_status ensure_local(tanq_sim* s, const FusedOp& op, const std::vector<Fused
     TRY(remap_swap(s, ab.first, ab.second));
   }
   return TANQ_OK;
-}
-
-void prof_begin(tanq_sim* s, Shard& sh, Prof& p) {
-  if (!s->prof_on || sh.id != s->rank0) return;
-  cudaEventCreate(&p.e0);
-  cudaEventCreate(&p.e1);
-  cudaEventRecord(p.e0, sh.stream);
-}
-void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
-  if (!s->prof_on || sh.id != s->rank0) return;
-  cudaEventRecord(p.e1, sh.stream);
-  s->prof.push_back(p);
 }
 
 tanq_status prof_flush(tanq_sim* s) {
@@ -976,6 +985,13 @@ tanq_status bind_op(const tanq_sim* s, const tanq_op& op, const tanq_noise_model
       out.S = mat_from(op.m, d * d);
     }
     if (!finite_mat(out.S)) return fail(TANQ_E_ARG, "non-finite matrix");
+    return TANQ_OK;
+  }
+  if (kind == TANQ_RESET) {  // {|0><0|, |0><1|}: noiseless, no calibration (reading R19)
+    Mat K0(2), K1(2);
+    K0(0, 0) = 1.0;
+    K1(0, 1) = 1.0;
+    out.S = superop_from_kraus({K0, K1});
     return TANQ_OK;
   }
   if ((kind == TANQ_RX || kind == TANQ_RY || kind == TANQ_RZ || kind == TANQ_CP) &&
@@ -1725,6 +1741,43 @@ tanq_status tanq_sample(tanq_sim* s, const tanq_readout* ro, uint64_t seed, uint
                            s0.stream));
   CUDA_TRY(cudaFreeAsync(dout, s0.stream));
   CUDA_TRY(cudaStreamSynchronize(s0.stream));
+  return TANQ_OK;
+}
+
+// Philox4x32-10 (same constants as the sampling kernel), first 53-bit uniform of (seed, 0).
+static double philox_uniform(uint64_t seed, uint64_t ctr) {
+  uint32_t c[4] = {(uint32_t)ctr, (uint32_t)(ctr >> 32), 0u, 0u};
+  uint32_t k[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k[0], n1 = lo1, n2 = hi0 ^ c[3] ^ k[1], n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    k[0] += 0x9E3779B9u;
+    k[1] += 0xBB67AE85u;
+  }
+  const uint64_t bits = (((uint64_t)c[0] << 21) ^ ((uint64_t)c[1] >> 11)) & ((1ull << 53) - 1);
+  return (double)bits * (1.0 / 9007199254740992.0);
+}
+
+tanq_status tanq_measure(tanq_sim* s, int qubit, uint64_t seed, int* outcome, double* prob) {
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  if (qubit < 0 || qubit >= s->n) return fail(TANQ_E_ARG, "qubit out of range");
+  double z = 0.0;
+  TRY(tanq_expect_pauli(s, 0, 1ull << qubit, &z, nullptr));  // <Z_q> = p0 - p1 (diagonal)
+  const double p1 = std::min(1.0, std::max(0.0, 0.5 * (1.0 - z)));
+  const int b = philox_uniform(seed, 0) < p1 ? 1 : 0;
+  const double pb = b ? p1 : 1.0 - p1;
+  if (pb < 1e-300) return fail(TANQ_E_STATE, "measured outcome has zero probability");
+  FusedOp op;  // superoperator of rho -> P_b rho P_b / p_b : only the (b,b) block survives
+  op.k = 1;
+  op.q[0] = qubit;
+  op.S = Mat(4);
+  op.S(3 * b, 3 * b) = 1.0 / pb;
+  TRY(apply_single(s, std::move(op)));
+  if (outcome) *outcome = b;
+  if (prob) *prob = pb;
   return TANQ_OK;
 }
 

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libtanq.so")
 
 KIND = {"id": 0, "x": 1, "y": 2, "z": 3, "h": 4, "s": 5, "sdg": 6, "t": 7, "tdg": 8, "sx": 9,
         "rx": 10, "ry": 11, "rz": 12, "cx": 13, "cz": 14, "cp": 15, "swap": 16,
-        "u": 17, "kraus": 18, "superop": 19}
+        "u": 17, "kraus": 18, "superop": 19, "reset": 20}
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_NOMEM", 3: "E_CUDA", 4: "E_NCCL", 5: "E_STATE",
           6: "E_UNSUPPORTED"}
 
@@ -117,6 +117,7 @@ SIGNATURES = {
     "tanq_probs": ([_P, ctypes.POINTER(tanq_readout), _P], _I),
     "tanq_expect_pauli": ([_P, _U64, _U64, _P, _P], _I),
     "tanq_sample": ([_P, ctypes.POINTER(tanq_readout), _U64, _U64, _P], _I),
+    "tanq_measure": ([_P, _I, _U64, ctypes.POINTER(_I), ctypes.POINTER(_D)], _I),
     "tanq_get_state": ([_P, _U64, _U64, _P], _I),
     "tanq_set_state": ([_P, _U64, _U64, _P], _I),
     "tanq_sync": ([_P], _I),
@@ -417,6 +418,13 @@ class Simulator:
         _check(lib().tanq_sample(self.h, ctypes.byref(ro.c) if ro else None, seed, shots,
                                  out.ctypes.data), "tanq_sample")
         return out
+
+    def measure(self, qubit: int, seed: int):
+        """Mid-circuit projective measurement: returns (outcome, probability of that outcome)."""
+        b, p = ctypes.c_int(), ctypes.c_double()
+        _check(lib().tanq_measure(self.h, qubit, seed, ctypes.byref(b), ctypes.byref(p)),
+               "tanq_measure")
+        return b.value, p.value
 
     # -- instrumentation --------------------------------------------------------------
     def profile(self) -> List[dict]:

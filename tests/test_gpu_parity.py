@@ -309,3 +309,42 @@ def test_plan_graph_replay(Sim):
         sim.set_state(dense.to_vec(rho0))
         plan.exec(sim)
         assert_parity(rho_of(sim, n), ref2)
+
+
+def test_reset_in_circuit(Sim):
+    c = W.random_circuit(5, 30, seed=77, kmax=2)
+    c.ops.insert(12, W.Op("reset", (2,)))
+    c.ops.append(W.Op("reset", (0,)))
+    nm = W.synthetic_calibration(c, 77)
+    with Sim(5) as sim:
+        sim.run_circuit(c, nm)
+        assert_parity(rho_of(sim, 5), dense.run(c, nm))
+
+
+def test_mid_circuit_measurement(Sim):
+    """tanq_measure: outcome probability from the diagonal, collapse P_b rho P_b / p_b."""
+    n = 5
+    c = W.random_circuit(n, 40, seed=88, kmax=2)
+    nm = W.synthetic_calibration(c, 88)
+    base = dense.run(c, nm)
+    p1 = float(sum(dense.probs(base, n)[x] for x in range(2 ** n) if (x >> 3) & 1))
+    ones = 0
+    for seed in range(40):
+        with Sim(n) as sim:
+            sim.run_circuit(c, nm)
+            b, pb = sim.measure(3, seed)
+            ones += b
+            assert abs(pb - (p1 if b else 1 - p1)) < 1e-12
+            ref = np.ascontiguousarray(base.copy())
+            P = np.diag([1.0 - b, float(b)]).astype(complex) / np.sqrt(pb)
+            dense.apply_kraus(ref, n, (3,), [P])
+            assert_parity(rho_of(sim, n), ref)
+            assert abs(np.trace(rho_of(sim, n)) - 1) < 1e-12
+    assert abs(ones - 40 * p1) <= 5 * np.sqrt(40 * p1 * (1 - p1)) + 1
+    # GHZ: measuring one qubit collapses all three
+    with Sim(3) as sim:
+        sim.run_circuit(W.ghz3())
+        b, pb = sim.measure(0, 123)
+        assert abs(pb - 0.5) < 1e-12
+        p = sim.probs()
+        assert abs(p[7 if b else 0] - 1.0) < 1e-12

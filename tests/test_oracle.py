@@ -366,3 +366,20 @@ def test_fused_channel_composition_matches_sequence():
     r2 = rho.copy()
     dense.apply_superop(r2, 4, qs, Sb @ Sa)
     assert np.abs(r1 - r2).max() < 1e-14
+
+
+def test_reset_channel():
+    """Reset = {|0><0|, |0><1|} (reading R19): |1><1| -> |0><0|; in general the qubit
+    ends in |0> and the rest is the partial trace over it."""
+    one = np.ascontiguousarray(_one_qubit_state([0, 1]).astype(complex))
+    _apply_ops(one, 1, [W.Op("reset", (0,))])
+    np.testing.assert_allclose(one, [[1, 0], [0, 0]], atol=1e-15)
+    rng = np.random.default_rng(12)
+    rho = np.ascontiguousarray(W.random_density(rng, 3))
+    r = rho.copy()
+    _apply_ops(r, 3, [W.Op("reset", (1,))])
+    t = rho.reshape(2, 2, 2, 2, 2, 2)                  # (q2, q1, q0 ; q2', q1', q0')
+    red = np.einsum("aibcid->abcd", t)                  # trace over qubit 1
+    ref = np.zeros((2, 2, 2, 2, 2, 2), dtype=complex)
+    ref[:, 0, :, :, 0, :] = red
+    np.testing.assert_allclose(r, ref.reshape(8, 8), atol=1e-15)

@@ -27,7 +27,7 @@ BASE_SEED = 240413184  # base seed 240413184 + config index
 
 # Gate names understood by both sides.  'u' carries a user matrix, 'kraus' a
 # user Kraus list, 'superop' a user superoperator (paper vec convention).
-ONE_Q = ("id", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "sx", "rx", "ry", "rz")
+ONE_Q = ("id", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "sx", "rx", "ry", "rz", "reset")
 TWO_Q = ("cx", "cz", "cp", "swap")
 MATRIX_KINDS = ("u", "kraus", "superop")
 
@@ -250,7 +250,7 @@ def synthetic_calibration(circ: Circuit, seed: int, depol: bool = True, thermal:
         qcal.append(QubitCal(t1 if thermal else 0.0, t2 if thermal else 0.0, p10, p01))
     nm = NoiseModel(n, qcal)
     keys = sorted({(op.kind, tuple(op.qubits)) for op in circ.ops
-                   if op.kind not in ("rz",) + MATRIX_KINDS})
+                   if op.kind not in ("rz", "reset") + MATRIX_KINDS})
     for kind, qs in keys:
         k = len(qs)
         if k == 1:

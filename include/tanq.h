@@ -257,6 +257,19 @@ tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const ta
 tanq_status tanq_sync(tanq_sim* s);
 const char* tanq_last_error(void);
 
+/* ---- OpenQASM 2.0 front-end (subset: qelib1 gates, qreg/creg, measure, reset, barrier;
+ *      no gate definitions / if) -- the paper's circuits arrive as QASM2 among other
+ *      front-ends and are transpiled to the device basis ---------------- */
+typedef struct tanq_qasm tanq_qasm;
+/* Parse; to_basis != 0 lowers every gate to {ID, SX, X, RZ, CX} (+ reset).  TANQ_E_ARG with
+ * "line L:C: ..." in tanq_last_error() on a syntax or semantic error. */
+tanq_status tanq_qasm_parse(const char* text, int to_basis, tanq_qasm** out);
+/* The parsed circuit; ops stay owned by the tanq_qasm and valid until tanq_qasm_free. */
+tanq_status tanq_qasm_circuit(const tanq_qasm* q, tanq_circuit* c, int* n_qubits, int* n_clbits);
+/* qubit measured into each classical bit (n_clbits entries), -1 if none. */
+tanq_status tanq_qasm_measures(const tanq_qasm* q, int32_t* qubit_of_clbit);
+tanq_status tanq_qasm_free(tanq_qasm* q);
+
 /* ---- instrumentation -------------------------------------------------------------- */
 /* Copy up to max entries of the per-kernel profile; returns count in *n_out. */
 tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* n_out);

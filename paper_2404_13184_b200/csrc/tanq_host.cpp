@@ -29,6 +29,11 @@ tanq_status fail(tanq_status s, const std::string& m) {
   g_err = m;
   return s;
 }
+}  // namespace
+
+void tanq::set_error(const char* msg) { g_err = msg; }
+
+namespace {
 
 // NCCL is loaded on demand (multi-process mode only) with dlopen: an already-loaded
 // libnccl.so.2 (e.g. the one torch brought in) is reused, so the library never pins an
@@ -1100,6 +1105,10 @@ tanq_status combine_probs(tanq_sim* s, DevScratch*& primary) {
     CUDA_TRY(cudaSetDevice(s0.device));
     NCCL_TRY(nccl().AllReduce(primary->probs, primary->probs, (size_t)1 << s->n, ncclDouble, ncclSum,
                            s->comm, s0.stream));
+    // every rank must take the same TANQ_E_STATE decision: max of |Im diag| over ranks (the
+    // bit patterns of non-negative doubles order like the values)
+    NCCL_TRY(nccl().AllReduce(primary->imax, primary->imax, 1, ncclUint64, ncclMax, s->comm,
+                              s0.stream));
   }
   // |Im diag| check
   double imx = 0.0;

@@ -6,6 +6,8 @@
 
 namespace tanq {
 
+void set_error(const char* msg);  // message returned by tanq_last_error() (thread-local)
+
 // A gate launch: apply a dense 4^K x 4^K complex matrix to every tuple of one shard.
 // Member i of a tuple sits at physical offset base + sum_j bit_j(i) << pos[j], where
 // pos[0] < pos[1] < ... < pos[2K-1] are the op's physical target bits (all local);

@@ -118,6 +118,10 @@ SIGNATURES = {
     "tanq_expect_pauli": ([_P, _U64, _U64, _P, _P], _I),
     "tanq_sample": ([_P, ctypes.POINTER(tanq_readout), _U64, _U64, _P], _I),
     "tanq_measure": ([_P, _I, _U64, ctypes.POINTER(_I), ctypes.POINTER(_D)], _I),
+    "tanq_qasm_parse": ([ctypes.c_char_p, _I, ctypes.POINTER(_P)], _I),
+    "tanq_qasm_circuit": ([_P, ctypes.POINTER(tanq_circuit), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "tanq_qasm_measures": ([_P, _P], _I),
+    "tanq_qasm_free": ([_P], _I),
     "tanq_get_state": ([_P, _U64, _U64, _P], _I),
     "tanq_set_state": ([_P, _U64, _U64, _P], _I),
     "tanq_sync": ([_P], _I),
@@ -292,6 +296,49 @@ class Plan:
             pass
 
 
+class QasmOp:
+    __slots__ = ("kind", "qubits", "theta", "mat", "kraus")
+
+    def __init__(self, kind, qubits, theta):
+        self.kind, self.qubits, self.theta, self.mat, self.kraus = kind, qubits, theta, None, None
+
+    def __repr__(self):
+        return f"QasmOp({self.kind}, {self.qubits}, {self.theta:.6g})"
+
+
+class QasmCircuit:
+    """tanq_qasm_parse: OpenQASM 2.0 subset -> circuit (optionally lowered to the IBM basis).
+    `.ops` mirrors the library's op list (kind names, qubits, angles) for inspection; runs use
+    the library-owned C array directly."""
+
+    def __init__(self, text: str, to_basis: bool = True):
+        h = ctypes.c_void_p()
+        _check(lib().tanq_qasm_parse(text.encode(), int(to_basis), ctypes.byref(h)), "tanq_qasm_parse")
+        self.h = h
+        c = tanq_circuit()
+        nq, nc = ctypes.c_int(), ctypes.c_int()
+        _check(lib().tanq_qasm_circuit(h, ctypes.byref(c), ctypes.byref(nq), ctypes.byref(nc)),
+               "tanq_qasm_circuit")
+        self.c, self.n, self.n_clbits = c, nq.value, nc.value
+        names = {v: k for k, v in KIND.items()}
+        self.ops = [QasmOp(names[c.ops[i].kind], tuple(c.ops[i].q[:c.ops[i].k]), c.ops[i].theta)
+                    for i in range(c.n_ops)]
+        meas = (ctypes.c_int32 * max(1, self.n_clbits))()
+        _check(lib().tanq_qasm_measures(h, meas), "tanq_qasm_measures")
+        self.measures = list(meas[:self.n_clbits])
+
+    def close(self):
+        if self.h:
+            lib().tanq_qasm_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().tanq_nccl_unique_id(buf, 128), "tanq_nccl_unique_id")
@@ -381,7 +428,12 @@ class Simulator:
 
     def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
                     profile: bool = False, prepared=None) -> dict:
-        cc = prepared[0] if prepared else CCircuit(circuit.ops)
+        if isinstance(circuit, QasmCircuit):
+            class _C:  # the library-owned op array
+                c = circuit.c
+            cc = _C()
+        else:
+            cc = prepared[0] if prepared else CCircuit(circuit.ops)
         cn = (prepared[1] if prepared else (CNoise(noise) if noise is not None else None))
         opts = tanq_run_opts(fuse, k_max, 0, 1 if profile else 0, 0)
         st = tanq_run_stats()

@@ -348,3 +348,26 @@ def test_mid_circuit_measurement(Sim):
         assert abs(pb - 0.5) < 1e-12
         p = sim.probs()
         assert abs(p[7 if b else 0] - 1.0) < 1e-12
+
+
+def test_qasm_front_end_on_gpu(Sim):
+    """A QASM2 program lowered to the IBM basis, bound to a calibration and run (NEXT-4)."""
+    from paper_2404_13184_b200 import QasmCircuit
+    src = """OPENQASM 2.0;
+include "qelib1.inc";
+qreg q[4];
+creg c[4];
+h q[0];
+cx q[0],q[1];
+cp(pi/3) q[1],q[2];
+u3(0.3,0.2,0.1) q[3];
+swap q[2],q[3];
+cz q[0],q[3];
+measure q -> c;
+"""
+    qc = QasmCircuit(src, to_basis=True)
+    circ = W.Circuit(qc.n, qc.ops)
+    nm = W.synthetic_calibration(circ, 17)
+    with Sim(qc.n) as sim:
+        sim.run_circuit(qc, nm)
+        assert_parity(rho_of(sim, qc.n), dense.run(circ, nm))

@@ -479,6 +479,7 @@ struct tanq_sim {
   size_t xchunk = 0;
   bool prof_on = false;
   std::vector<Prof> prof;
+  std::vector<cudaEvent_t> event_pool;  // recycled timing events (no create per launch)
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_bytes[4] = {0, 0, 0, 0};
   double prof_flops[4] = {0, 0, 0, 0};
@@ -555,10 +556,21 @@ tanq_status stream_wait(const Shard& waiter, const Shard& on) {
   return TANQ_OK;
 }
 
+cudaEvent_t pooled_event(tanq_sim* s) {
+  if (!s->event_pool.empty()) {
+    cudaEvent_t e = s->event_pool.back();
+    s->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
 void prof_begin(tanq_sim* s, Shard& sh, Prof& p) {
   if (!s->prof_on || sh.id != s->rank0) return;
-  cudaEventCreate(&p.e0);
-  cudaEventCreate(&p.e1);
+  p.e0 = pooled_event(s);
+  p.e1 = pooled_event(s);
   cudaEventRecord(p.e0, sh.stream);
 }
 void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
@@ -705,8 +717,8 @@ tanq_status prof_flush(tanq_sim* s) {
     s->prof_flops[p.cls] += p.flops;
     s->prof_hw_flops[p.cls] += p.hw_flops;
     s->prof_launches[p.cls]++;
-    cudaEventDestroy(p.e0);
-    cudaEventDestroy(p.e1);
+    s->event_pool.push_back(p.e0);
+    s->event_pool.push_back(p.e1);
   }
   s->prof.clear();
   return TANQ_OK;
@@ -1283,6 +1295,7 @@ tanq_status tanq_destroy(tanq_sim* s) {
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
   }
+  for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
   for (auto& sh : s->shards) {
     cudaSetDevice(sh.device);
     if (sh.stream) cudaStreamSynchronize(sh.stream);

@@ -127,7 +127,8 @@ typedef struct {
  * with the B200 cost model (default).  k_max in {1,2,3} (default 3: 3-qubit groups).  chunk_bytes: remap staging chunk
  * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
  * on single-shard handles capture their launches into a CUDA graph on the first
- * tanq_plan_exec and replay it afterwards (ignored with bit0). */
+ * tanq_plan_exec and replay it afterwards (ignored with bit0); bit2 = disable the
+ * Hermitian mirror mode for this run. */
 typedef struct {
   int32_t fuse;
   int32_t k_max;
@@ -256,6 +257,14 @@ tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const ta
 
 tanq_status tanq_sync(tanq_sim* s);
 const char* tanq_last_error(void);
+
+/* Mirror mode: while rho is known to be Hermitian and an op is
+ * Hermiticity-preserving (every Kraus-form op; user superoperators are checked), single-shard
+ * handles read and compute only one tuple of each transpose pair and write the other as its
+ * conjugate (24 instead of 32 B per amplitude, half the FP64 work).  rho is known Hermitian
+ * after create / reset; tanq_set_state clears it; this call measures max|rho - rho^dag| and
+ * sets it when <= tol * max(1, max|rho|).  Disable with env TANQ_MIRROR=0 or run flag bit2. */
+tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm);
 
 /* ---- OpenQASM 2.0 front-end (subset: qelib1 gates, qreg/creg, measure, reset, barrier;
  *      no gate definitions / if) -- the paper's circuits arrive as QASM2 among other

@@ -258,6 +258,20 @@ Mat embed_superop(const Mat& Ss, const std::vector<int>& pos, int k) {
   return S;
 }
 
+// Hermiticity preservation of a superoperator in the vec convention l = r + c d: the map
+// sends X^dag to E(X)^dag iff S[(r',c'),(r,c)] = conj(S[(c',r'),(c,r)]).  Every Kraus form
+// has it; user superoperators are checked.
+bool is_herm_preserving(const Mat& S, int k) {
+  const int d = 1 << k, D = d * d;
+  for (int l2 = 0; l2 < D; ++l2)
+    for (int l = 0; l < D; ++l) {
+      const int t2 = (l2 % d) * d + l2 / d, t = (l % d) * d + l / d;
+      const cd a = S(l2, l), b = std::conj(S(t2, t));
+      if (std::abs(a - b) > 1e-14 * (1.0 + std::abs(a))) return false;
+    }
+  return true;
+}
+
 // ------------------------------------------------------------------------------------
 // ops, fusion
 // ------------------------------------------------------------------------------------
@@ -266,6 +280,7 @@ struct FusedOp {
   int q[3] = {0, 0, 0};
   Mat S;            // 4^k, local index over q[0..k-1] (for a factored group: the dense product)
   int parts = 1;    // number of pre-fusion ops folded in
+  bool herm = true;  // Hermiticity-preserving: S[(r',c'),(r,c)] = conj S[(c',r'),(c,r)]
   std::vector<FusedOp> sub;  // k=3 factored group: sub-ops applied in order in one pass
 };
 
@@ -302,6 +317,7 @@ FusedOp merge(const FusedOp& Q, const FusedOp& G) {
       if (U.q[i] == G.q[j]) pg.push_back(i);
   U.S = matmul(embed_superop(G.S, pg, U.k), embed_superop(Q.S, pq, U.k));
   U.parts = Q.parts + G.parts;
+  U.herm = Q.herm && G.herm;
   return U;
 }
 
@@ -328,6 +344,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
           if (same) {
             Q.S = matmul(G.S, Q.S);
             Q.parts += G.parts;
+            Q.herm = Q.herm && G.herm;
             continue;
           }
         } else {
@@ -402,6 +419,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
     FusedOp out = g.op;
     out.S = embed_superop(acc.S, pos, g.op.k);
     out.parts = acc.parts;
+    out.herm = acc.herm;
     return out;
   };
   std::vector<FusedOp> out;
@@ -423,7 +441,10 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
                          prog <= (size_t)tanq::kGroupProgMax;
     if (fact_ok && fact <= dense && fact < sep) {
       FusedOp f = g.op;  // factored: S formed only on export (tanq_plan_get_op)
-      for (int m : g.members) f.sub.push_back(l1[m]);
+      for (int m : g.members) {
+        f.sub.push_back(l1[m]);
+        f.herm = f.herm && l1[m].herm;
+      }
       out.push_back(std::move(f));
     } else if (dense < sep) {
       out.push_back(dense_of(g));
@@ -480,6 +501,9 @@ struct tanq_sim {
   bool prof_on = false;
   std::vector<Prof> prof;
   std::vector<cudaEvent_t> event_pool;  // recycled timing events (no create per launch)
+  bool herm_state = true;   // rho known Hermitian (create / reset; cleared by set_state and
+                            // by non-Hermiticity-preserving ops; tanq_check_hermitian sets it)
+  bool mirror_allowed = true;  // env TANQ_MIRROR=0 disables the mirror mode
   double prof_ms[4] = {0, 0, 0, 0};
   double prof_bytes[4] = {0, 0, 0, 0};
   double prof_flops[4] = {0, 0, 0, 0};
@@ -760,6 +784,17 @@ std::vector<double2> member_order_S(const FusedOp& op, const MemberMap& mm) {
   return out;
 }
 
+// Mirror mode: rho known Hermitian, op Hermiticity-preserving, one shard with
+// the initial interleaved layout (row/col bits of every qubit adjacent), whole 16-tuple blocks.
+bool use_mirror(const tanq_sim* s, const FusedOp& op) {
+  if (!s->mirror_allowed || !s->herm_state || !op.herm || s->shards.size() != 1 || s->dist)
+    return false;
+  for (int i = 0; i < 2 * s->n; ++i)
+    if (s->phys[i] != (uint32_t)i) return false;
+  const int tuple_bits = s->L - 2 * op.k;
+  return op.k == 1 ? tuple_bits >= 2 : tuple_bits >= 4;
+}
+
 size_t group_prog_elems(const FusedOp& op) {
   if (op.sub.empty()) return tanq::group_frag_elems(3);
   size_t e = 0;
@@ -776,6 +811,7 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
     p.lo_mask[t] = ((uint64_t)1 << tile.bits[t].first) - 1;
   }
   p.n_tuples = (uint64_t)1 << (s->L - 6);
+  p.mirror = use_mirror(s, op) ? 1u : 0u;
   std::vector<const FusedOp*> subs;
   if (op.sub.empty())
     subs.push_back(&op);
@@ -846,7 +882,11 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   }
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
-    Prof pr{k - 1, nullptr, nullptr, 32.0 * amps, flops_amp * amps, hw_amp * amps};
+    // mirror mode reads only the canonical half of the tuples: 24 B / amplitude, half the flops
+    const bool mir = k < 3 ? use_mirror(s, op) : gp->mirror != 0;
+    const double fr = mir ? 0.5 : 1.0;
+    Prof pr{k - 1, nullptr, nullptr, (mir ? 24.0 : 32.0) * amps, fr * flops_amp * amps,
+            fr * hw_amp * amps};
     prof_begin(s, sh, pr);
     if (k == 1) {
       tanq::GateParams<1> p;
@@ -856,6 +896,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
         p.lo_mask[t] = ((uint64_t)1 << mm.bits[t].first) - 1;
       }
       p.n_tuples = n_tuples;
+      p.mirror = mir ? 1u : 0u;
       CUDA_TRY(tanq::launch_gate1(sh.data, p, sh.stream));
     } else if (k == 2) {
       tanq::GateParams<2> p;
@@ -865,6 +906,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
         p.lo_mask[t] = ((uint64_t)1 << mm.bits[t].first) - 1;
       }
       p.n_tuples = n_tuples;
+      p.mirror = mir ? 1u : 0u;
       CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
     } else {
       int di = 0;
@@ -877,6 +919,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
     s->launches++;
     prof_end(s, sh, pr);
   }
+  if (!op.herm) s->herm_state = false;
   return TANQ_OK;
 }
 
@@ -1000,6 +1043,7 @@ tanq_status bind_op(const tanq_sim* s, const tanq_op& op, const tanq_noise_model
       out.S = superop_from_kraus(Ks);
     } else {
       out.S = mat_from(op.m, d * d);
+      out.herm = is_herm_preserving(out.S, k);
     }
     if (!finite_mat(out.S)) return fail(TANQ_E_ARG, "non-finite matrix");
     return TANQ_OK;
@@ -1191,6 +1235,11 @@ static tanq_status create_common(int n, tanq_sim* s) {
         }
       }
   reset_layout(s);
+  {
+    const char* mv = getenv("TANQ_MIRROR");
+    s->mirror_allowed = !(mv && mv[0] == '0');
+  }
+  s->herm_state = true;
   return TANQ_OK;
 }
 
@@ -1334,6 +1383,7 @@ tanq_status tanq_reset(tanq_sim* s) {
     s->launches++;
   }
   reset_layout(s);
+  s->herm_state = true;
   return TANQ_OK;
 }
 
@@ -1415,6 +1465,7 @@ tanq_status tanq_apply_superop(tanq_sim* s, int k, const int* qubits, const tanq
   for (int j = 0; j < k; ++j) op.q[j] = qubits[j];
   op.S = mat_from(S, 1 << (2 * k));
   if (!finite_mat(op.S)) return fail(TANQ_E_ARG, "non-finite matrix");
+  op.herm = is_herm_preserving(op.S, k);
   return apply_single(s, std::move(op));
 }
 
@@ -1432,6 +1483,7 @@ struct tanq_plan {
     const tanq_sim* sim = nullptr;
     const double2* data = nullptr;
     uint32_t phys[64];
+    bool herm = false, mirror = false;
     cudaGraphExec_t exec = nullptr;
     double2* dprog = nullptr;
     int device = -1;
@@ -1453,7 +1505,8 @@ namespace {
 tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
   Shard& sh = s->shards[0];
   auto& g = p->g;
-  const bool hit = g.exec && g.sim == s && g.data == sh.data &&
+  const bool hit = g.exec && g.sim == s && g.data == sh.data && g.herm == s->herm_state &&
+                   g.mirror == s->mirror_allowed &&
                    std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0;
   CUDA_TRY(cudaSetDevice(sh.device));
   if (!hit) {
@@ -1488,6 +1541,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     int di = 0;
     for (size_t i = 0; i < s->scratch.size(); ++i)
       if (s->scratch[i].device == sh.device) di = (int)i;
+    const bool herm0 = s->herm_state;
     cudaGraph_t graph;
     CUDA_TRY(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal));
     const uint64_t l0 = s->launches;
@@ -1514,10 +1568,14 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     s->launches = l0;
     g.sim = s;
     g.data = sh.data;
+    g.herm = herm0;
+    g.mirror = s->mirror_allowed;
     std::memcpy(g.phys, s->phys, sizeof(g.phys));
   }
   CUDA_TRY(cudaGraphLaunch(g.exec, sh.stream));
   s->launches += g.kernels;
+  for (const auto& op : p->ops)
+    if (!op.herm) s->herm_state = false;
   return TANQ_OK;
 }
 }  // namespace
@@ -1644,6 +1702,8 @@ tanq_status tanq_plan_exec(tanq_sim* s, const tanq_plan* p, tanq_run_stats* st) 
   for (const auto& f : p->ops)
     if (2 * f.k > s->L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
   const uint64_t r0 = s->remap_count, b0 = s->remap_bytes;
+  const bool mirror_saved = s->mirror_allowed;
+  if (p->flags & 4) s->mirror_allowed = false;
   tanq_status r;
   if ((p->flags & 2) && s->shards.size() == 1 && !s->dist && !(p->flags & 1)) {
     r = exec_graph(s, p);
@@ -1652,6 +1712,7 @@ tanq_status tanq_plan_exec(tanq_sim* s, const tanq_plan* p, tanq_run_stats* st) 
     r = exec_ops(s, p->ops);
     s->prof_on = false;
   }
+  s->mirror_allowed = mirror_saved;
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->ops_in = p->ops_in;
@@ -1878,7 +1939,33 @@ tanq_status tanq_get_state(tanq_sim* s, uint64_t first, uint64_t count, tanq_c64
 
 tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const tanq_c64* in) {
   if (!s || (!in && count)) return fail(TANQ_E_ARG, "NULL argument");
+  s->herm_state = false;  // unknown until tanq_check_hermitian
   return state_io(s, first, count, nullptr, in);
+}
+
+tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm) {
+  if (!s || !is_herm) return fail(TANQ_E_ARG, "NULL argument");
+  *is_herm = 0;
+  if (s->shards.size() != 1 || s->dist) return TANQ_OK;  // transpose pairs span shards
+  for (int i = 0; i < 2 * s->n; ++i)
+    if (s->phys[i] != (uint32_t)i) return TANQ_OK;
+  Shard& sh = s->shards[0];
+  DevScratch& d = scratch_for(s, sh.device);
+  TRY(ensure_scratch(s, d));
+  CUDA_TRY(cudaSetDevice(sh.device));
+  unsigned long long* res = reinterpret_cast<unsigned long long*>(d.scal);  // [diff, maxabs]
+  CUDA_TRY(cudaMemsetAsync(res, 0, 2 * sizeof(unsigned long long), sh.stream));
+  CUDA_TRY(tanq::launch_herm_check(sh.data, s->L, res, sh.stream));
+  s->launches++;
+  unsigned long long h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, sh.stream));
+  CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  double diff, mx;
+  std::memcpy(&diff, &h[0], sizeof(double));
+  std::memcpy(&mx, &h[1], sizeof(double));
+  *is_herm = diff <= tol * std::max(1.0, mx) ? 1 : 0;
+  s->herm_state = *is_herm != 0;
+  return TANQ_OK;
 }
 
 tanq_status tanq_sync(tanq_sim* s) {

@@ -20,6 +20,7 @@ struct GateParams {
   uint64_t lo_mask[2 * K];   // (1 << pos[j]) - 1
   uint64_t n_tuples;         // 2^(L - 2K)
   uint32_t pos[2 * K];
+  uint32_t mirror;           // 1: Hermitian mirror mode
 };
 
 // K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 64-member tuples (6 physical
@@ -40,6 +41,7 @@ struct GroupParams {
   uint64_t lo_mask[6];
   uint64_t n_tuples;
   uint32_t pos[6];
+  uint32_t mirror;           // 1: Hermitian mirror mode
   GroupSub sub[kMaxSub];
 };
 
@@ -94,5 +96,7 @@ cudaError_t launch_cdf(const double* p, double* cdf, int n, cudaStream_t st);
 cudaError_t launch_sample(const double* cdf, int n, uint64_t seed, uint64_t shots,
                           unsigned long long* out, cudaStream_t st);
 cudaError_t launch_add(double* dst, const double* src, uint64_t count, cudaStream_t st);
+// res[0] = max |a[P] - conj(a[pair_swap(P)])|, res[1] = max |a[P]| (bit patterns of doubles)
+cudaError_t launch_herm_check(const double2* a, int L, unsigned long long* res, cudaStream_t st);
 
 }  // namespace tanq

@@ -37,6 +37,15 @@ __device__ __forceinline__ uint64_t insert_zeros(uint64_t t, const uint64_t* lo,
   return t;
 }
 
+// Hermitian mirror (DESIGN.md §5 "mirror mode"): with the interleaved single-shard layout
+// the row / column bits of every qubit are adjacent, so the transpose position of a tuple
+// index (or of a member index) swaps each adjacent bit pair.  rho' Hermitian gives
+// rho'[mirror] = conj(rho'[element]).
+__device__ __forceinline__ uint64_t pair_swap(uint64_t x) {
+  return ((x & 0x5555555555555555ull) << 1) | ((x >> 1) & 0x5555555555555555ull);
+}
+__device__ __forceinline__ double2 cj(double2 v) { return make_double2(v.x, -v.y); }
+
 __device__ __forceinline__ void ld32(const double2* p, double2& a, double2& b) {
   asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
@@ -65,6 +74,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__host__ __device__ constexpr int pswap_c(int i) {
+  return ((i & 0x55) << 1) | ((i >> 1) & 0x55);
+}
+
 // ------------------------------------------------------------------------------------
 // K1 / K2: FMA register stream
 // ------------------------------------------------------------------------------------
@@ -74,10 +87,19 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
   constexpr int M = 1 << (2 * K);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.n_tuples; t += stride) {
-    uint64_t base = t;
+    uint64_t tm = t;
+    if (p.mirror) {  // only the canonical tuple of each transpose pair is read and computed
+      tm = pair_swap(t);
+      if (tm < t) continue;
+    }
+    uint64_t base = t, basem = tm;
 #pragma unroll
-    for (int j = 0; j < 2 * K; ++j) base = ((base & ~p.lo_mask[j]) << 1) | (base & p.lo_mask[j]);
+    for (int j = 0; j < 2 * K; ++j) {
+      base = ((base & ~p.lo_mask[j]) << 1) | (base & p.lo_mask[j]);
+      basem = ((basem & ~p.lo_mask[j]) << 1) | (basem & p.lo_mask[j]);
+    }
     double2* ptr = a + base;
+    double2* ptrm = a + basem;
     uint64_t off[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -117,6 +139,10 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
         ptr[off[l]] = y[0];
         ptr[off[l + 1]] = y[1];
       }
+      if (tm != t) {  // transpose tuple: conj, member bit pairs swapped
+        ptrm[off[pswap_c(l)]] = cj(y[0]);
+        ptrm[off[pswap_c(l + 1)]] = cj(y[1]);
+      }
     }
   }
 }
@@ -130,8 +156,10 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
 //   D fragment = member 8mt + (lane>>2) of tuples 2(lane&3), 2(lane&3)+1 -> one 32 B store
 //   when consecutive tuples are adjacent in memory (physical bit 0 not a target).
 // The next tile's loads are issued before the current tile's DMMAs (register prefetch).
+// Mirror mode (Hermitian rho, Hermiticity-preserving S): only canonical 16-tuple blocks are
+// read and computed; every result is also written, conjugated, to its transpose position.
 // ------------------------------------------------------------------------------------
-template <bool ADJ, int PF>
+template <bool ADJ>
 __global__ void __launch_bounds__(256, 2)
     gate2_mma_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<2> p) {
   const int lane = threadIdx.x & 31;
@@ -180,20 +208,33 @@ __global__ void __launch_bounds__(256, 2)
     }
   };
 
-  // register ring of PF + 1 tiles: tile i is computed while tiles i+1..i+PF are in flight
-  double2 xr[PF + 1][4];
-  uint64_t tile = warp;
+  // mirror mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
+  auto valid = [&](uint64_t tl) {
+    if (!p.mirror) return true;
+    const uint64_t b = tl >> 1;
+    return b <= pair_swap(b);
+  };
+  auto next_tile = [&](uint64_t tl) {
+    while (tl < n_tiles && !valid(tl)) tl += nwarps;
+    return tl;
+  };
+  uint64_t offDm[2];
 #pragma unroll
-  for (int s = 0; s < PF; ++s) load_tile(tile + (uint64_t)s * nwarps, xr[s]);
-  for (; tile < n_tiles; tile += nwarps) {
-    load_tile(tile + (uint64_t)PF * nwarps, xr[PF]);
+  for (int mt = 0; mt < 2; ++mt) offDm[mt] = member_off(pswap_c(8 * mt + r4));
+
+  double2 xb_cur[4], xb_nxt[4];
+  uint64_t tile = next_tile(warp);
+  load_tile(tile, xb_cur);
+  while (tile < n_tiles) {
+    const uint64_t nxt = next_tile(tile + nwarps);
+    load_tile(nxt, xb_nxt);  // register prefetch of the next tile
     double p1[2][2], p2[2][2], p3[2][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
       p1[mt][0] = p1[mt][1] = p2[mt][0] = p2[mt][1] = p3[mt][0] = p3[mt][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const double2 xb = xr[0][ks];
+      const double2 xb = xb_cur[ks];
       const double xs = xb.x + xb.y;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
@@ -203,6 +244,7 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
     const uint64_t t0 = tile * 8 + 2 * c4;
+    const bool mir = p.mirror && (tile >> 1) != pair_swap(tile >> 1);
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const double2 y0 = make_double2(p1[mt][0] - p2[mt][0], p3[mt][0] - p1[mt][0] - p2[mt][0]);
@@ -217,11 +259,14 @@ __global__ void __launch_bounds__(256, 2)
         if (t0 < p.n_tuples) a[base_of(t0) + offD[mt]] = y0;
         if (t0 + 1 < p.n_tuples) a[base_of(t0 + 1) + offD[mt]] = y1;
       }
+      if (mir) {  // whole blocks only: n_tuples is a multiple of 16 in mirror mode
+        a[base_of(pair_swap(t0)) + offDm[mt]] = cj(y0);
+        a[base_of(pair_swap(t0 + 1)) + offDm[mt]] = cj(y1);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < PF; ++s)
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) xr[s][ks] = xr[s + 1][ks];
+    for (int ks = 0; ks < 4; ++ks) xb_cur[ks] = xb_nxt[ks];
+    tile = nxt;
   }
 }
 
@@ -252,22 +297,10 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
   const uint64_t cap = 148ull * 16;  // one wave: 2 CTAs x 8 warps per SM, persistent
   if (warps > cap) warps = cap;
   unsigned grid = (unsigned)((warps + 7) / 8);
-  static int pf = -1;
-  if (pf < 0) {
-    const char* e = getenv("TANQ_K2_PF");
-    pf = (e && e[0] == '2') ? 2 : 1;
-  }
-  if (pf == 2) {
-    if (p.pos[0] == 0)
-      gate2_mma_kernel<false, 2><<<grid, 256, 0, st>>>(a, p);
-    else
-      gate2_mma_kernel<true, 2><<<grid, 256, 0, st>>>(a, p);
-  } else {
-    if (p.pos[0] == 0)
-      gate2_mma_kernel<false, 1><<<grid, 256, 0, st>>>(a, p);
-    else
-      gate2_mma_kernel<true, 1><<<grid, 256, 0, st>>>(a, p);
-  }
+  if (p.pos[0] == 0)
+    gate2_mma_kernel<false><<<grid, 256, 0, st>>>(a, p);
+  else
+    gate2_mma_kernel<true><<<grid, 256, 0, st>>>(a, p);
   return cudaGetLastError();
 }
 
@@ -431,25 +464,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   double2* sProg = reinterpret_cast<double2*>(smem_raw);
   double2* sX = sProg + kGroupProgMax;
   // copy mapping tables: iteration i (16) -> (tuple bits, member bits, address offset)
-  uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + WARPS * NBUF * 512);
-  int* sIterTM = reinterpret_cast<int*>(sIterOff + 16);
-  GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 16);
+  uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + WARPS * NBUF * 512);  // [2][16]
+  int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);                          // [2][16]
+  GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // The 9 index bits of a tile element (3 tuple bits at the lowest free physical positions,
   // 6 member bits at pos[]) sorted by physical position: lanes take the 5 lowest, the copy
   // iterations the next 4, so every copy instruction covers the most contiguous addresses.
-  int bit_pos[9], bit_id[9];  // id < 3: tuple bit, else member bit id-3
+  // Mirror mode writes each element (t, m) conjugated to its transpose position: tuple bit j
+  // lands on free position f[j^1] (pairs (0,1), (2,3)), member bit j on pos[j^1].
+  int freep[4];
   {
     int nf = 0;
-    for (int f = 0; f < 64 && nf < 3; ++f) {
+    for (int f = 0; f < 64 && nf < 4; ++f) {
       bool tgt = false;
       for (int j = 0; j < 6; ++j) tgt |= (int)p.pos[j] == f;
-      if (!tgt) bit_pos[nf++] = f;
+      if (!tgt) freep[nf++] = f;
     }
-    for (int j = 0; j < 3; ++j) bit_id[j] = j;
+  }
+  auto build_map = [&](bool mir, int& ltm, uint64_t& loff, int* it_tm, uint64_t* it_off) {
+    int bit_pos[9], bit_id[9];  // id < 3: tuple bit, else member bit id-3
+    for (int j = 0; j < 3; ++j) {
+      bit_pos[j] = freep[mir ? (j ^ 1) : j];
+      bit_id[j] = j;
+    }
     for (int j = 0; j < 6; ++j) {
-      bit_pos[3 + j] = (int)p.pos[j];
+      bit_pos[3 + j] = (int)p.pos[mir ? (j ^ 1) : j];
       bit_id[3 + j] = 3 + j;
     }
     for (int x = 1; x < 9; ++x)  // insertion sort by position
@@ -457,34 +498,39 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         int tp = bit_pos[y]; bit_pos[y] = bit_pos[y - 1]; bit_pos[y - 1] = tp;
         int ti = bit_id[y]; bit_id[y] = bit_id[y - 1]; bit_id[y - 1] = ti;
       }
-  }
-  auto tm_of = [&](int bits, int first, int cnt, uint64_t& off) {
-    int t = 0, m = 0;
-    off = 0;
-    for (int b = 0; b < cnt; ++b)
-      if ((bits >> b) & 1) {
-        const int id = bit_id[first + b];
-        if (id < 3) t |= 1 << id; else m |= 1 << (id - 3);
-        off += (uint64_t)1 << bit_pos[first + b];
-      }
-    return t | (m << 3);
+    auto tm_of = [&](int bits, int first, int cnt, uint64_t& off) {
+      int t = 0, m = 0;
+      off = 0;
+      for (int b = 0; b < cnt; ++b)
+        if ((bits >> b) & 1) {
+          const int id = bit_id[first + b];
+          if (id < 3) t |= 1 << id; else m |= 1 << (id - 3);
+          off += (uint64_t)1 << bit_pos[first + b];
+        }
+      return t | (m << 3);
+    };
+    ltm = tm_of(lane, 0, 5, loff);
+    if (threadIdx.x < 16) it_tm[threadIdx.x] = tm_of(threadIdx.x, 5, 4, it_off[threadIdx.x]);
   };
   // address of (tile, t, m) = base(tile*8) + deposit(t at free bits) + deposit(m at pos[]):
   // insert_zeros is a bit deposit, so the tuple and member parts add independently.
-  uint64_t lane_off;
-  const int lane_tm = tm_of(lane, 0, 5, lane_off);
-  if (threadIdx.x < 16) {
-    uint64_t o;
-    sIterTM[threadIdx.x] = tm_of(threadIdx.x, 5, 4, o);
-    sIterOff[threadIdx.x] = o;
-  }
+  int lane_tm, mlane_tm = 0;
+  uint64_t lane_off, mlane_off = 0;
+  build_map(false, lane_tm, lane_off, sIterTM, sIterOff);
+  if (p.mirror) build_map(true, mlane_tm, mlane_off, sIterTM + 16, sIterOff + 16);
   for (int e = threadIdx.x; e < p.prog_elems; e += blockDim.x) sProg[e] = p.prog[e];
   for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
   __syncthreads();
 
   const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
   const uint64_t tile_stride = (uint64_t)gridDim.x * WARPS;
-  uint64_t tile = (uint64_t)blockIdx.x * WARPS + warp;
+  // mirror mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
+  auto next_tile = [&](uint64_t tl) {
+    if (p.mirror)
+      while (tl < n_tiles && (tl >> 1) > pair_swap(tl >> 1)) tl += (uint64_t)gridDim.x * WARPS;
+    return tl;
+  };
+  uint64_t tile = next_tile((uint64_t)blockIdx.x * WARPS + warp);
   double2* const wbuf = sX + warp * NBUF * 512;  // NBUF 512-double2 tiles (no indexed array:
                                                   // a dynamically indexed pointer array spills)
   // element (lane, i): tuple t = tm & 7, member m = tm >> 3, address base(tile*8) + off
@@ -509,9 +555,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   if (NBUF == 2 && tile < n_tiles) issue_load(tile, wbuf);
   int cur = 0;
-  for (; tile < n_tiles; tile += tile_stride) {
+  for (; tile < n_tiles; tile = next_tile(tile + tile_stride)) {
     if constexpr (NBUF == 2) {
-      const uint64_t next = tile + tile_stride;
+      const uint64_t next = next_tile(tile + tile_stride);
       if (next < n_tiles) {
         issue_load(next, wbuf + ((cur ^ 1) << 9));
         cp_async_wait<1>();
@@ -545,6 +591,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         elem(i, t, m, off);
         if (tile * 8 + t < p.n_tuples) dst[off] = X[xs_idx(m, t)];
       }
+      if (p.mirror && (tile >> 1) != pair_swap(tile >> 1)) {  // conj to transpose positions
+        double2* dstm = a + insert_zeros(pair_swap(tile * 8), p.lo_mask, 6);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int tm = mlane_tm | sIterTM[16 + i];
+          dstm[mlane_off + sIterOff[16 + i]] = cj(X[xs_idx(tm >> 3, tm & 7)]);
+        }
+      }
     }
     __syncwarp();
     cur ^= 1;
@@ -555,7 +609,7 @@ template <int WARPS, int NBUF, bool HAS3, int UI>
 static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
   static bool attr_set = false;
   const size_t smem = (size_t)kGroupProgMax * sizeof(double2) +
-                      (size_t)WARPS * NBUF * 512 * sizeof(double2) + 16 * 8 + 16 * 4 +
+                      (size_t)WARPS * NBUF * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
                       (size_t)kMaxSub * sizeof(GroupSub);
   auto kern = group3_kernel<WARPS, NBUF, HAS3, UI>;
   if (!attr_set) {
@@ -839,6 +893,31 @@ __global__ void add_kernel(double* dst, const double* src, uint64_t count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride)
     dst[i] += src[i];
 }
+__global__ void herm_check_kernel(const double2* __restrict__ a, uint64_t N,
+                                  unsigned long long* res) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double d = 0.0, m = 0.0;
+  for (uint64_t P = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; P < N; P += stride) {
+    const double2 x = a[P], y = a[pair_swap(P)];
+    d = fmax(d, fmax(fabs(x.x - y.x), fabs(x.y + y.y)));
+    m = fmax(m, fmax(fabs(x.x), fabs(x.y)));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(res, (unsigned long long)__double_as_longlong(d));
+    atomicMax(res + 1, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+cudaError_t launch_herm_check(const double2* a, int L, unsigned long long* res, cudaStream_t st) {
+  const uint64_t N = (uint64_t)1 << L;
+  herm_check_kernel<<<grid_for(N, kThreads, 148ull * 8), kThreads, 0, st>>>(a, N, res);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add(double* dst, const double* src, uint64_t count, cudaStream_t st) {
   add_kernel<<<grid_for(count, kThreads, 148ull * 8), kThreads, 0, st>>>(dst, src, count);
   return cudaGetLastError();

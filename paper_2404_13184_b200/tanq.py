@@ -122,6 +122,7 @@ SIGNATURES = {
     "tanq_qasm_circuit": ([_P, ctypes.POINTER(tanq_circuit), ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "tanq_qasm_measures": ([_P, _P], _I),
     "tanq_qasm_free": ([_P], _I),
+    "tanq_check_hermitian": ([_P, _D, ctypes.POINTER(_I)], _I),
     "tanq_get_state": ([_P, _U64, _U64, _P], _I),
     "tanq_set_state": ([_P, _U64, _U64, _P], _I),
     "tanq_sync": ([_P], _I),
@@ -234,10 +235,11 @@ class Plan:
     over world_size shards."""
 
     def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
-                 world_size: int = 1, graph: bool = False):
+                 world_size: int = 1, graph: bool = False, mirror: bool = True):
         cc = CCircuit(circuit.ops)
         cn = CNoise(noise) if noise is not None else None
-        opts = tanq_run_opts(fuse, k_max, 0, (1 if profile else 0) | (2 if graph else 0), 0)
+        opts = tanq_run_opts(fuse, k_max, 0,
+                             (1 if profile else 0) | (2 if graph else 0) | (0 if mirror else 4), 0)
         h = ctypes.c_void_p()
         nmp = ctypes.byref(cn.c) if cn is not None else None
         if sim is None:
@@ -405,6 +407,11 @@ class Simulator:
         v = _c64_array(vec).reshape(-1)
         _check(lib().tanq_set_state(self.h, first, v.size, v.ctypes.data), "tanq_set_state")
 
+    def check_hermitian(self, tol: float = 1e-13) -> bool:
+        r = ctypes.c_int()
+        _check(lib().tanq_check_hermitian(self.h, tol, ctypes.byref(r)), "tanq_check_hermitian")
+        return bool(r.value)
+
     def sync(self):
         _check(lib().tanq_sync(self.h), "tanq_sync")
 
@@ -427,7 +434,7 @@ class Simulator:
                "tanq_apply_superop")
 
     def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
-                    profile: bool = False, prepared=None) -> dict:
+                    profile: bool = False, prepared=None, mirror: bool = True) -> dict:
         if isinstance(circuit, QasmCircuit):
             class _C:  # the library-owned op array
                 c = circuit.c
@@ -435,7 +442,7 @@ class Simulator:
         else:
             cc = prepared[0] if prepared else CCircuit(circuit.ops)
         cn = (prepared[1] if prepared else (CNoise(noise) if noise is not None else None))
-        opts = tanq_run_opts(fuse, k_max, 0, 1 if profile else 0, 0)
+        opts = tanq_run_opts(fuse, k_max, 0, (1 if profile else 0) | (0 if mirror else 4), 0)
         st = tanq_run_stats()
         _check(lib().tanq_run_circuit(self.h, ctypes.byref(cc.c),
                                       ctypes.byref(cn.c) if cn is not None else None,
@@ -443,8 +450,9 @@ class Simulator:
         return st.as_dict()
 
     def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
-             profile: bool = False, graph: bool = False) -> "Plan":
-        return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile, graph=graph)
+             profile: bool = False, graph: bool = False, mirror: bool = True) -> "Plan":
+        return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile, graph=graph,
+                    mirror=mirror)
 
     @staticmethod
     def prepare(circuit, noise=None):

@@ -28,16 +28,17 @@ def main():
         st = torch.cuda.Stream()
         torch.cuda.set_stream(st)
         sim.set_stream(st.cuda_stream)
+        import workloads as W
         for qs in cases:
             k = len(qs)
-            S = (rng.standard_normal((4 ** k, 4 ** k)) + 1j * rng.standard_normal((4 ** k, 4 ** k))) * 0.1
+            Ks = W.random_kraus(rng, 2 ** k, 2)  # CPTP: Hermiticity-preserving (mirror mode)
             for _ in range(3):
-                sim.apply_superop(qs, S)
+                sim.apply_channel(qs, Ks)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             for _ in range(args.reps):
-                sim.apply_superop(qs, S)
+                sim.apply_channel(qs, Ks)
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.reps
@@ -45,13 +46,11 @@ def main():
             tf = 8 * 4 ** k * amps / (ms * 1e-3) / 1e12
             out.append({"qubits": qs, "k": k, "ms": ms, "GBs": gbs, "alg_TFs": tf})
             print(json.dumps(out[-1]), flush=True)
-        # K3 groups: chains of k=2 superoperators inside 3 qubits, one pass (fuse=2, k_max=3)
-        import workloads as W
+        # K3 groups: chains of k=2 channels inside 3 qubits, one pass (fuse=2, k_max=3)
         groups = [[(0, 1), (1, 2)], [(1, 2), (2, 3), (1, 3)], [(5, n - 1), (n - 1, n - 2)],
                   [(0, 1), (1, 2), (0, 2), (2, 1)], [(3, 7), (7, n - 1), (3, n - 1), (7, 3), (3, 7)]]
         for g in groups:
-            ops = [W.Op("superop", qs, mat=(rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))) * 0.1)
-                   for qs in g]
+            ops = [W.Op("kraus", qs, kraus=W.random_kraus(rng, 4, 2)) for qs in g]
             plan = sim.plan(W.Circuit(n, ops), None, fuse=2, k_max=3)
             info = plan.info()
             for _ in range(3):

@@ -130,13 +130,14 @@ def test_apply_gate_and_channel(Sim, n, qubits):
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("fuse,kmax", [(0, 2), (1, 2), (2, 2), (2, 3)])
-def test_random_noisy_circuits(Sim, seed, fuse, kmax):
+@pytest.mark.parametrize("mirror", [True, False])
+def test_random_noisy_circuits(Sim, seed, fuse, kmax, mirror):
     n = 3 + seed
     c = W.random_circuit(n, 50, seed=500 + seed, kmax=3)
     nm = W.synthetic_calibration(c, seed, depol=True, thermal=True, overrot=True)
     nm.order = seed % 2
     with Sim(n) as sim:
-        sim.run_circuit(c, nm, fuse=fuse, k_max=kmax)
+        sim.run_circuit(c, nm, fuse=fuse, k_max=kmax, mirror=mirror)
         got = rho_of(sim, n)
     assert_parity(got, dense.run(c, nm))
 
@@ -371,3 +372,32 @@ measure q -> c;
     with Sim(qc.n) as sim:
         sim.run_circuit(qc, nm)
         assert_parity(rho_of(sim, qc.n), dense.run(circ, nm))
+
+
+
+def test_mirror_mode_state_tracking(Sim):
+    """Hermitian mirror mode: used only while rho is known Hermitian and ops preserve it."""
+    n = 6
+    rng = np.random.default_rng(31)
+    c = W.random_circuit(n, 40, seed=31, kmax=3)
+    nm = W.synthetic_calibration(c, 31)
+    rho = W.random_density(rng, n, rank=5)
+    ref = dense.run(c, nm, rho=np.ascontiguousarray(rho.copy()))
+    with Sim(n) as sim:
+        sim.set_state(dense.to_vec(rho))
+        assert sim.check_hermitian()
+        sim.run_circuit(c, nm)
+        assert_parity(rho_of(sim, n), ref)
+        # a non-Hermitian state is detected and handled without the mirror
+        X = W.random_complex(rng, (2 ** n, 2 ** n)) * 0.01
+        sim.set_state(dense.to_vec(X))
+        assert not sim.check_hermitian()
+        sim.run_circuit(c, nm)
+        ref2 = dense.run(c, nm, rho=np.ascontiguousarray(X.copy()))
+        assert np.abs(rho_of(sim, n) - ref2).max() < 1e-12
+        # a non-Hermiticity-preserving superoperator in the middle of a circuit
+        sim.reset()
+        S = W.random_complex(rng, (16, 16)) * 0.2
+        c2 = W.Circuit(n, c.ops[:20] + [W.Op("superop", (1, 4), mat=S)] + c.ops[20:])
+        sim.run_circuit(c2, nm)
+        assert_parity(rho_of(sim, n), dense.run(c2, nm))

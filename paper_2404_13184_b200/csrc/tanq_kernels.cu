@@ -455,14 +455,14 @@ __device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const
 // WARPS warps per CTA (one CTA per SM), NBUF tile buffers per warp (2 = cp.async double
 // buffering), HAS3: the program may contain a dense k=3 sub-op (needs the register budget of
 // 8 warps), UI: sub-tuples per k=2 pass.
-template <int WARPS, int NBUF, bool HAS3, int UI>
+template <int WARPS, int NBUF, bool HAS3, int UI, int PMAX>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     group3_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // shared: program (<= kGroupProgMax double2) | X tiles WARPS x NBUF x 512 double2 (128 KiB) |
   //         copy tables | sub-op headers
   double2* sProg = reinterpret_cast<double2*>(smem_raw);
-  double2* sX = sProg + kGroupProgMax;
+  double2* sX = sProg + PMAX;
   // copy mapping tables: iteration i (16) -> (tuple bits, member bits, address offset)
   uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + WARPS * NBUF * 512);  // [2][16]
   int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);                          // [2][16]
@@ -605,13 +605,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-template <int WARPS, int NBUF, bool HAS3, int UI>
+template <int WARPS, int NBUF, bool HAS3, int UI, int PMAX = kGroupProgMax>
 static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
   static bool attr_set = false;
-  const size_t smem = (size_t)kGroupProgMax * sizeof(double2) +
+  const size_t smem = (size_t)PMAX * sizeof(double2) +
                       (size_t)WARPS * NBUF * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
                       (size_t)kMaxSub * sizeof(GroupSub);
-  auto kern = group3_kernel<WARPS, NBUF, HAS3, UI>;
+  auto kern = group3_kernel<WARPS, NBUF, HAS3, UI, PMAX>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -632,13 +632,15 @@ cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
   bool has3 = false;
   for (int i = 0; i < p.n_sub; ++i) has3 |= p.sub[i].k == 3;
   if (has3) return launch_group3_cfg<8, 2, true, 4>(a, p, st);
-  static int cfg = -1;  // TANQ_G3=a|b|c selects the factored-group configuration
+  static int cfg = -1;  // TANQ_G3=a|b|c|d selects the factored-group configuration
   if (cfg < 0) {
     const char* e = getenv("TANQ_G3");
-    cfg = e ? (e[0] - 'a') : 2;
+    cfg = e ? (e[0] - 'a') : 1;
   }
   if (cfg == 0) return launch_group3_cfg<8, 2, false, 4>(a, p, st);
   if (cfg == 2) return launch_group3_cfg<16, 1, false, 1>(a, p, st);
+  if (cfg == 3 && p.prog_elems <= 2048)  // small programs: 12 warps, cp.async double buffer
+    return launch_group3_cfg<12, 2, false, 2, 2048>(a, p, st);
   return launch_group3_cfg<16, 1, false, 2>(a, p, st);
 }
 

@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic", default="profiles/ncu_traffic.json")
     ap.add_argument("--n", type=int, required=True, help="qubits of the captured run (alg bytes = 32*4^n)")
+    ap.add_argument("--bytes-per-amp", type=float, default=32.0,
+                    help="algorithmic bytes per amplitude of the captured launches (24 in mirror mode)")
     ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,group3=group_k3_dmma")
     args = ap.parse_args()
     nmap = [kv.split("=") for kv in args.name_map.split(",")]
@@ -65,7 +67,7 @@ def main():
                 tb = to_bytes(r[rd], units[rd]) + to_bytes(r[wr], units[wr])
                 for pat, short in nmap:
                     if pat in name:
-                        alg = 32.0 * 4 ** args.n
+                        alg = args.bytes_per_amp * 4 ** args.n
                         traffic[short] = {"dram_bytes_per_launch": tb, "algorithmic_bytes_per_launch": alg,
                                           "ratio": tb / alg, "n_qubits": args.n,
                                           "source": os.path.basename(rep)}

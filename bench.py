@@ -330,7 +330,7 @@ def run_ours(args):
                        "n_qubits": n, "gates": len(c.ops), "gate_updates": ops,
                        "kernel_ops": st["ops_fused"],
                        "fusion": f"fuse={args.fuse} k_max={args.kmax}",
-                       "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"]],
+                       "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
                        "remaps_per_step": st["n_remaps"],
                        "state_bytes": 16 * 4 ** n, "shard_bytes": info["shard_bytes"],
                        "parallelism": (f"state partitioned over {world} GPU(s) by high bits"
@@ -370,7 +370,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--fuse", type=int, default=2)
-    ap.add_argument("--kmax", type=int, default=3)
+    ap.add_argument("--kmax", type=int, default=4)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1,

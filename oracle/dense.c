@@ -19,7 +19,7 @@
 
 typedef double complex cplx;
 
-#define MAXD 8 /* 2^k, k <= 3 */
+#define MAXD 16 /* 2^k, k <= 4 */
 
 static uint64_t spread_bits(uint64_t i, int k, const int* q) {
   uint64_t v = 0;

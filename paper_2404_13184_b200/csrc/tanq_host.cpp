@@ -277,7 +277,7 @@ bool is_herm_preserving(const Mat& S, int k) {
 // ------------------------------------------------------------------------------------
 struct FusedOp {
   int k = 0;
-  int q[3] = {0, 0, 0};
+  int q[4] = {0, 0, 0, 0};  // k <= 3 for ops; a factored group may span 4 qubits
   Mat S;            // 4^k, local index over q[0..k-1] (for a factored group: the dense product)
   int parts = 1;    // number of pre-fusion ops folded in
   bool herm = true;  // Hermiticity-preserving: S[(r',c'),(r,c)] = conj S[(c',r'),(c,r)]
@@ -367,6 +367,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   if (mode == 1) return pass(in, 2, true);
   std::vector<FusedOp> l1 = pass(in, std::min(kmax, 2), false);
   if (kmax < 3) return l1;
+  const int glim = std::min(kmax, 4);  // group qubits: 3, or 4 (factored groups only)
   // 3-qubit grouping: greedy groups of <= 3 qubits over the k<=2 ops; a group replaces its
   // members only when their summed pass cost exceeds one dense k=3 pass.
   struct Group {
@@ -384,14 +385,17 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
       }
     if (idx >= 0) {
       Group& Q = groups[idx];
-      int uq[3], uk = Q.op.k;
+      bool has3 = G.k == 3;
+      for (int m : Q.members) has3 |= l1[m].k == 3;
+      const int lim = has3 ? 3 : glim;  // dense k=3 sub-ops only run on 3-qubit tiles
+      int uq[4], uk = Q.op.k;
       for (int i = 0; i < Q.op.k; ++i) uq[i] = Q.op.q[i];
       bool fits = true;
       for (int j = 0; j < G.k && fits; ++j) {
         bool f = false;
         for (int i = 0; i < uk; ++i) f |= uq[i] == G.q[j];
         if (!f) {
-          if (uk == 3) fits = false; else uq[uk++] = G.q[j];
+          if (uk >= lim) fits = false; else uq[uk++] = G.q[j];
         }
       }
       if (fits) {
@@ -424,7 +428,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   };
   std::vector<FusedOp> out;
   for (Group& g : groups) {
-    if (g.members.size() == 1 || g.op.k < 3) {
+    if (g.members.size() == 1 || g.op.k < 3) {  // k<=2 unions were merged by level 1
       for (int m : g.members) out.push_back(l1[m]);
       continue;
     }
@@ -436,7 +440,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
       prog += l1[m].k == 3 ? 4096 : (l1[m].k == 2 ? 256 : 16);
     }
     fact = std::max(1.0, kGroupBase + fact);
-    const double dense = sep_cost(3);
+    const double dense = g.op.k == 3 ? sep_cost(3) : 1e30;
     const bool fact_ok = g.members.size() <= (size_t)tanq::kMaxSub &&
                          prog <= (size_t)tanq::kGroupProgMax;
     if (fact_ok && fact <= dense && fact < sep) {
@@ -460,7 +464,7 @@ struct Prof {
   cudaEvent_t e0, e1;
   double bytes, flops, hw_flops;
 };
-const char* kProfNames[] = {"gate_k1", "gate_k2", "group_k3_dmma", "remap"};
+const char* kProfNames[] = {"gate_k1", "gate_k2", "group_dmma", "remap"};
 
 }  // namespace
 
@@ -791,7 +795,7 @@ bool use_mirror(const tanq_sim* s, const FusedOp& op) {
     return false;
   for (int i = 0; i < 2 * s->n; ++i)
     if (s->phys[i] != (uint32_t)i) return false;
-  const int tuple_bits = s->L - 2 * op.k;
+  const int tuple_bits = s->L - 2 * op.k;  // groups: op.k = tile qubits (3 or 4)
   return op.k == 1 ? tuple_bits >= 2 : tuple_bits >= 4;
 }
 
@@ -805,12 +809,14 @@ size_t group_prog_elems(const FusedOp& op) {
 // Build the K3 group program (sub-op headers + fragment-ordered matrices) for the current
 // layout; returns the kernel parameters except `prog`.
 void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, double2* prog) {
-  const MemberMap tile = member_map(s, 3, op.q);
-  for (int t = 0; t < 6; ++t) {
-    p.pos[t] = (uint32_t)tile.bits[t].first;
-    p.lo_mask[t] = ((uint64_t)1 << tile.bits[t].first) - 1;
+  const int TBITS = 2 * op.k;  // 6 (3-qubit tile) or 8 (4-qubit tile)
+  const MemberMap tile = member_map(s, op.k, op.q);
+  p.nq = op.k;
+  for (int t = 0; t < 8; ++t) {
+    p.pos[t] = t < TBITS ? (uint32_t)tile.bits[t].first : 63u;
+    p.lo_mask[t] = t < TBITS ? ((uint64_t)1 << tile.bits[t].first) - 1 : 0;
   }
-  p.n_tuples = (uint64_t)1 << (s->L - 6);
+  p.n_tuples = (uint64_t)1 << (s->L - TBITS);
   p.mirror = use_mirror(s, op) ? 1u : 0u;
   std::vector<const FusedOp*> subs;
   if (op.sub.empty())
@@ -827,11 +833,11 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
     g.k = sb.k;
     g.s_off = (int)off;
     // tile bit index of each of the sub-op's sorted physical positions
-    int tb[6], nb = 0, rb[6], nr = 0;
+    int tb[8], nb = 0, rb[8], nr = 0;
     for (int t = 0; t < 2 * sb.k; ++t)
-      for (int u = 0; u < 6; ++u)
+      for (int u = 0; u < TBITS; ++u)
         if (tile.bits[u].first == mm.bits[t].first) tb[nb++] = u;
-    for (int u = 0; u < 6; ++u) {
+    for (int u = 0; u < TBITS; ++u) {
       bool used = false;
       for (int t = 0; t < nb; ++t) used |= tb[t] == u;
       if (!used) rb[nr++] = u;
@@ -857,8 +863,8 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
   p.prog_elems = (int)off;
 }
 
-// Launch one fused op on every shard (targets must be local).  For k = 3, `prog` holds the
-// group program already copied to each device (indexed like s->scratch).
+// Launch one fused op on every shard (targets must be local).  For k >= 3 (groups), `prog`
+// holds the group program already copied to each device (indexed like s->scratch).
 tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* gp,
                       const std::vector<const double2*>* prog) {
   const int k = op.k, M = 1 << (2 * k);
@@ -866,7 +872,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   const double amps = (double)((uint64_t)1 << s->L);
   // algorithmic: 8 flops per complex MAC; executed: K1 (FMA) 8, K2 / K3 (3-multiply DMMA) 6
   double flops_amp = 8.0 * M, hw_amp = (k == 1 ? 8.0 : 6.0) * M;
-  if (k == 3 && !op.sub.empty()) {
+  if (k >= 3 && !op.sub.empty()) {
     flops_amp = hw_amp = 0;
     for (const auto& sb : op.sub) {
       const int Ms = 1 << (2 * sb.k);
@@ -883,10 +889,10 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
     // mirror mode reads only the canonical half of the tuples: 24 B / amplitude, half the flops
-    const bool mir = k < 3 ? use_mirror(s, op) : gp->mirror != 0;
+    const bool mir = k < 3 ? use_mirror(s, op) : gp->mirror != 0;  // groups: k = 3 or 4
     const double fr = mir ? 0.5 : 1.0;
-    Prof pr{k - 1, nullptr, nullptr, (mir ? 24.0 : 32.0) * amps, fr * flops_amp * amps,
-            fr * hw_amp * amps};
+    Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 24.0 : 32.0) * amps,
+            fr * flops_amp * amps, fr * hw_amp * amps};
     prof_begin(s, sh, pr);
     if (k == 1) {
       tanq::GateParams<1> p;
@@ -938,7 +944,7 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   // into a persistent pinned host buffer and copied (async) to each device before the launch.
   size_t total = 0;
   for (const auto& op : ops)
-    if (op.k == 3) total += group_prog_elems(op);
+    if (op.k >= 3) total += group_prog_elems(op);
   if (total) {
     for (auto& sh : s->shards) {
       DevScratch& d = scratch_for(s, sh.device);
@@ -960,7 +966,7 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   for (size_t i = 0; i < ops.size(); ++i) {
     const FusedOp& op = ops[i];
     TRY(ensure_local(s, op, &ops, i + 1));
-    if (op.k != 3) {
+    if (op.k < 3) {
       TRY(launch_op(s, op, nullptr, nullptr));
       continue;
     }
@@ -1522,12 +1528,12 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     }
     size_t total = 0;
     for (const auto& op : p->ops)
-      if (op.k == 3) total += group_prog_elems(op);
+      if (op.k >= 3) total += group_prog_elems(op);
     std::vector<double2> host(total ? total : 1);
     std::vector<tanq::GroupParams> gps;
     size_t off = 0;
     for (const auto& op : p->ops)
-      if (op.k == 3) {
+      if (op.k >= 3) {
         gps.emplace_back();
         build_group(s, op, gps.back(), host.data() + off);
         off += gps.back().prog_elems;
@@ -1549,7 +1555,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     size_t gi = 0;
     tanq_status st = TANQ_OK;
     for (const auto& op : p->ops) {
-      if (op.k != 3) {
+      if (op.k < 3) {
         st = launch_op(s, op, nullptr, nullptr);
       } else {
         ptr[di] = g.dprog + off;
@@ -1587,10 +1593,11 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   if (!c || !out) return fail(TANQ_E_ARG, "NULL argument");
   *out = nullptr;
   if (c->n_ops && !c->ops) return fail(TANQ_E_ARG, "ops is NULL");
-  tanq_run_opts opts{2, 3, 0, 0, 0};
+  tanq_run_opts opts{2, 4, 0, 0, 0};
   if (o) opts = *o;
   if (opts.fuse < 0 || opts.fuse > 2) return fail(TANQ_E_ARG, "fuse must be 0, 1 or 2");
-  if (opts.k_max < 1 || opts.k_max > 3) return fail(TANQ_E_ARG, "k_max must be 1..3");
+  if (opts.k_max < 1 || opts.k_max > 4) return fail(TANQ_E_ARG, "k_max must be 1..4");
+  if (opts.k_max == 4 && L < 10) opts.k_max = 3;  // 4-qubit tiles need 8 member bits + tuples
   if (opts.k_max == 3 && L < 6) opts.k_max = 2;
   const auto t0 = std::chrono::steady_clock::now();
   tanq_sim shape;  // only n and L are read by the validators

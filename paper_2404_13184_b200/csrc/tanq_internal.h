@@ -23,24 +23,25 @@ struct GateParams {
   uint32_t mirror;           // 1: Hermitian mirror mode
 };
 
-// K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 64-member tuples (6 physical
-// bits pos[], all local) in one HBM round trip.  Sub-op matrices live in `prog` in A-fragment
+// K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 4^nq-member tuples (2 nq
+// physical bits pos[], all local, nq = 3 or 4) in one HBM round trip.  Sub-op matrices live in `prog` in A-fragment
 // order (group_make_frags); mi[i] / mu[u] map sub-op member i / sub-tuple u to tile members.
 static constexpr int kMaxSub = 40;
 static constexpr int kGroupProgMax = 5632;  // double2 (88 KiB): one dense k=3 + 6 k=2, or 22 k=2
 struct GroupSub {
   int32_t k;
   int32_t s_off;     // offset of the sub-op matrix in prog (double2 units)
-  uint8_t mi[16];
-  uint8_t mu[16];
+  uint8_t mi[16];    // tile member of sub-op member i
+  uint8_t mu[64];    // tile member offset of sub-tuple u (4^(NQ-k) sub-tuples)
 };
 struct GroupParams {
   const double2* prog;
   int32_t prog_elems;
   int32_t n_sub;
-  uint64_t lo_mask[6];
+  int32_t nq;                // group qubits: 3 (64-member tuples) or 4 (256-member tuples)
+  uint64_t lo_mask[8];
   uint64_t n_tuples;
-  uint32_t pos[6];
+  uint32_t pos[8];
   uint32_t mirror;           // 1: Hermitian mirror mode
   GroupSub sub[kMaxSub];
 };

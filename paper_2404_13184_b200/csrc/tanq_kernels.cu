@@ -32,7 +32,7 @@ static inline unsigned grid_for(uint64_t work, int threads, uint64_t cap = 148ul
 
 __device__ __forceinline__ uint64_t insert_zeros(uint64_t t, const uint64_t* lo, int cnt) {
 #pragma unroll
-  for (int j = 0; j < 6; ++j)
+  for (int j = 0; j < 8; ++j)
     if (j < cnt) t = ((t & ~lo[j]) << 1) | (t & lo[j]);
   return t;
 }
@@ -305,25 +305,31 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------
-// K3: 3-qubit groups on DMMA.8x8x4 (mma.sync.m8n8k4 f64).
+// K3: 3- and 4-qubit groups on DMMA.8x8x4 (mma.sync.m8n8k4 f64).
 //
-// One HBM round trip per group: a warp stages a tile of 8 tuples x 64 members (the group's
-// 6 physical bits) in shared memory with cp.async (double-buffered), runs the group's
-// program of sub-ops on the tile, and writes the tile back.  Sub-ops:
-//   k=3  dense 64x64 superoperator (the fused k=3 op of SURVEY A-5): Y[64x8] = S X.
-//   k=2  16x16 superoperator on the 4 sub-tuples of each tuple: Y[16x32] = S X[16x32].
-//   k=1  4x4 superoperator on the 16 sub-tuples (FMA).
+// One HBM round trip per group: a warp stages a tile of 512 amplitudes -- T tuples x 4^NQ
+// members, the group's 2*NQ physical bits (NQ = 3: 8 x 64, NQ = 4: 2 x 256) -- in shared
+// memory with cp.async, runs the group's program of sub-ops on the tile, and writes the tile
+// back.  Sub-ops:
+//   k=3  dense 64x64 superoperator (NQ = 3 only; the fused k=3 op of SURVEY A-5): Y = S X.
+//   k=2  16x16 superoperator on the 4^(NQ-2) sub-tuples of each tuple: Y[16x32] = S X[16x32].
+//   k=1  4x4 superoperator on the 4^(NQ-1) sub-tuples (FMA).
 // Complex products use three real GEMMs: P1 = Sr Xr, P2 = Si Xi, P3 = (Sr+Si)(Xr+Xi);
 // Yr = P1 - P2, Yi = P3 - P1 - P2 (25% fewer FP64 ops than the paper's 4-MMA scheme).
 // Fragments (PTX m8n8k4 .row.col f64): A[8x4] lane -> (lane>>2, lane&3);
 // B[4x8] lane -> (k = lane&3, n = lane>>2); D[8x8] lane -> (lane>>2, 2*(lane&3)+{0,1}).
+// The 32 columns of a k=2 sub-op are (sub-tuple u, tuple t): col = u*T + t.
 // Sub-op matrices are stored in A-fragment order by the host (group_make_*).
 // ------------------------------------------------------------------------------------
-static constexpr int kGWarps = 8;
 
-// Tile element (member m, tuple t) lives at m*8 + (t ^ (m & 7)) (XOR swizzle): conflict-free
-// for both the tuple-major fragment reads and the address-ordered global<->shared copies.
-__device__ __forceinline__ int xs_idx(int m, int t) { return m * 8 + (t ^ (m & 7)); }
+// Tile element (member m, tuple t), linear e = m*T + t, lives at e ^ ((e >> 3) & 7) (XOR
+// swizzle; for NQ = 3 this is m*8 + (t ^ (m & 7))): conflict-free tuple-major fragment reads
+// and address-ordered global<->shared copies.
+template <int T>
+__device__ __forceinline__ int xs_idx(int m, int t) {
+  const int e = m * T + t;
+  return e ^ ((e >> 3) & 7);
+}
 
 size_t group_frag_elems(int k) { return k == 3 ? 4096 : (k == 2 ? 256 : 16); }
 
@@ -342,13 +348,14 @@ void group_make_frags(int k, const double2* S, double2* frag) {
 }
 
 __device__ __forceinline__ void group_sub_k3(double2* X, const double2* F, int lane) {
+  // NQ = 3 only (T = 8): tile members are the sub-op members
   const int r4 = lane >> 2, c4 = lane & 3;
   double p1[8][2], p2[8][2], p3[8][2];
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) p1[mt][0] = p1[mt][1] = p2[mt][0] = p2[mt][1] = p3[mt][0] = p3[mt][1] = 0.0;
 #pragma unroll 4
   for (int ks = 0; ks < 16; ++ks) {
-    const double2 xb = X[xs_idx(ks * 4 + c4, r4)];
+    const double2 xb = X[xs_idx<8>(ks * 4 + c4, r4)];
     const double xs = xb.x + xb.y;
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -363,13 +370,14 @@ __device__ __forceinline__ void group_sub_k3(double2* X, const double2* F, int l
   for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
     for (int c = 0; c < 2; ++c)
-      X[xs_idx(mt * 8 + r4, 2 * c4 + c)] =
+      X[xs_idx<8>(mt * 8 + r4, 2 * c4 + c)] =
           make_double2(p1[mt][c] - p2[mt][c], p3[mt][c] - p1[mt][c] - p2[mt][c]);
 }
 
-template <int UI>  // sub-tuples processed at once (1, 2 or 4): ILP vs registers
+template <int T, int UI>  // T tuples per tile; UI n-tiles (of 8 columns) processed at once
 __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const uint8_t* mi,
                                              const uint8_t* mu, int lane) {
+  constexpr int TB = T == 8 ? 3 : 1;
   const int r4 = lane >> 2, c4 = lane & 3;
   double sr[2][4], si[2][4], ss[2][4];
 #pragma unroll
@@ -387,10 +395,19 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) md[mt] = mi[8 * mt + r4];
 #pragma unroll
-  for (int u0 = 0; u0 < 4; u0 += UI) {
-    int mo[UI];
+  for (int n0 = 0; n0 < 4; n0 += UI) {
+    int mob[UI], tb[UI];  // B column of this lane in n-tile n0+u: (u, t) = (col >> TB, col % T)
 #pragma unroll
-    for (int u = 0; u < UI; ++u) mo[u] = mu[u0 + u];
+    for (int u = 0; u < UI; ++u) {
+      if constexpr (T == 8) {  // col >> 3 = n-tile, col & 7 = r4
+        mob[u] = mu[n0 + u];
+        tb[u] = r4;
+      } else {
+        const int col = (n0 + u) * 8 + r4;
+        mob[u] = mu[col >> TB];
+        tb[u] = col & (T - 1);
+      }
+    }
     double p1[UI][2][2], p2[UI][2][2], p3[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
@@ -401,7 +418,7 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
     for (int ks = 0; ks < 4; ++ks) {
       double2 xb[UI];
 #pragma unroll
-      for (int u = 0; u < UI; ++u) xb[u] = X[xs_idx(mb[ks] | mo[u], r4)];
+      for (int u = 0; u < UI; ++u) xb[u] = X[xs_idx<T>(mb[ks] | mob[u], tb[u])];
 #pragma unroll
       for (int u = 0; u < UI; ++u) {
         const double xs = xb[u].x + xb[u].y;
@@ -415,28 +432,33 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
     }
     __syncwarp();
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int u = 0; u < UI; ++u)
 #pragma unroll
-      for (int u = 0; u < UI; ++u)
+      for (int c = 0; c < 2; ++c) {
+        const int col = (n0 + u) * 8 + 2 * c4 + c;
+        const int mo = T == 8 ? mob[u] : mu[col >> TB], t = col & (T - 1);
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          X[xs_idx(md[mt] | mo[u], 2 * c4 + c)] = make_double2(
+        for (int mt = 0; mt < 2; ++mt)
+          X[xs_idx<T>(md[mt] | mo, t)] = make_double2(
               p1[u][mt][c] - p2[u][mt][c], p3[u][mt][c] - p1[u][mt][c] - p2[u][mt][c]);
+      }
     __syncwarp();
   }
 }
 
+template <int T>
 __device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const uint8_t* mi,
                                              const uint8_t* mu, int lane) {
+  constexpr int TB = T == 8 ? 3 : 1;
   double2 S[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) S[i] = F[i];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int col = lane + 32 * j, u = col >> 3, t = col & 7;
+    const int col = lane + 32 * j, mo = mu[col >> TB], t = col & (T - 1);
     double2 x[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = X[xs_idx(mi[i] | mu[u], t)];
+    for (int i = 0; i < 4; ++i) x[i] = X[xs_idx<T>(mi[i] | mo, t)];
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
       double yr = 0.0, yi = 0.0;
@@ -447,19 +469,20 @@ __device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const
         yi = fma(S[l * 4 + m].x, x[m].y, yi);
         yi = fma(S[l * 4 + m].y, x[m].x, yi);
       }
-      X[xs_idx(mi[l] | mu[u], t)] = make_double2(yr, yi);
+      X[xs_idx<T>(mi[l] | mo, t)] = make_double2(yr, yi);
     }
   }
 }
 
-// WARPS warps per CTA (one CTA per SM), NBUF tile buffers per warp (2 = cp.async double
-// buffering), HAS3: the program may contain a dense k=3 sub-op (needs the register budget of
-// 8 warps), UI: sub-tuples per k=2 pass.
-template <int WARPS, int NBUF, bool HAS3, int UI, int PMAX>
+// NQ group qubits, WARPS warps per CTA (one CTA per SM), NBUF tile buffers per warp
+// (2 = cp.async double buffering), HAS3: the program may contain a dense k=3 sub-op (needs
+// the register budget of 8 warps), UI: n-tiles per k=2 pass, PMAX: program capacity.
+template <int NQ, int WARPS, int NBUF, bool HAS3, int UI, int PMAX>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-    group3_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
+    group_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
+  constexpr int MB = 2 * NQ, TB = 9 - MB, T = 1 << TB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // shared: program (<= kGroupProgMax double2) | X tiles WARPS x NBUF x 512 double2 (128 KiB) |
+  // shared: program (<= PMAX double2) | X tiles WARPS x NBUF x 512 double2 |
   //         copy tables | sub-op headers
   double2* sProg = reinterpret_cast<double2*>(smem_raw);
   double2* sX = sProg + PMAX;
@@ -469,29 +492,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // The 9 index bits of a tile element (3 tuple bits at the lowest free physical positions,
-  // 6 member bits at pos[]) sorted by physical position: lanes take the 5 lowest, the copy
+  // The 9 index bits of a tile element (TB tuple bits at the lowest free physical positions,
+  // MB member bits at pos[]) sorted by physical position: lanes take the 5 lowest, the copy
   // iterations the next 4, so every copy instruction covers the most contiguous addresses.
   // Mirror mode writes each element (t, m) conjugated to its transpose position: tuple bit j
-  // lands on free position f[j^1] (pairs (0,1), (2,3)), member bit j on pos[j^1].
+  // lands on free position f[j^1], member bit j on pos[j^1].
   int freep[4];
   {
     int nf = 0;
     for (int f = 0; f < 64 && nf < 4; ++f) {
       bool tgt = false;
-      for (int j = 0; j < 6; ++j) tgt |= (int)p.pos[j] == f;
+      for (int j = 0; j < MB; ++j) tgt |= (int)p.pos[j] == f;
       if (!tgt) freep[nf++] = f;
     }
   }
   auto build_map = [&](bool mir, int& ltm, uint64_t& loff, int* it_tm, uint64_t* it_off) {
-    int bit_pos[9], bit_id[9];  // id < 3: tuple bit, else member bit id-3
-    for (int j = 0; j < 3; ++j) {
+    int bit_pos[9], bit_id[9];  // id < TB: tuple bit, else member bit id-TB
+    for (int j = 0; j < TB; ++j) {
       bit_pos[j] = freep[mir ? (j ^ 1) : j];
       bit_id[j] = j;
     }
-    for (int j = 0; j < 6; ++j) {
-      bit_pos[3 + j] = (int)p.pos[mir ? (j ^ 1) : j];
-      bit_id[3 + j] = 3 + j;
+    for (int j = 0; j < MB; ++j) {
+      bit_pos[TB + j] = (int)p.pos[mir ? (j ^ 1) : j];
+      bit_id[TB + j] = TB + j;
     }
     for (int x = 1; x < 9; ++x)  // insertion sort by position
       for (int y = x; y > 0 && bit_pos[y] < bit_pos[y - 1]; --y) {
@@ -504,15 +527,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       for (int b = 0; b < cnt; ++b)
         if ((bits >> b) & 1) {
           const int id = bit_id[first + b];
-          if (id < 3) t |= 1 << id; else m |= 1 << (id - 3);
+          if (id < TB) t |= 1 << id; else m |= 1 << (id - TB);
           off += (uint64_t)1 << bit_pos[first + b];
         }
-      return t | (m << 3);
+      return t | (m << TB);
     };
     ltm = tm_of(lane, 0, 5, loff);
     if (threadIdx.x < 16) it_tm[threadIdx.x] = tm_of(threadIdx.x, 5, 4, it_off[threadIdx.x]);
   };
-  // address of (tile, t, m) = base(tile*8) + deposit(t at free bits) + deposit(m at pos[]):
+  // address of (tile, t, m) = base(tile*T) + deposit(t at free bits) + deposit(m at pos[]):
   // insert_zeros is a bit deposit, so the tuple and member parts add independently.
   int lane_tm, mlane_tm = 0;
   uint64_t lane_off, mlane_off = 0;
@@ -522,33 +545,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
   __syncthreads();
 
-  const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
+  const uint64_t n_tiles = (p.n_tuples + T - 1) >> TB;
   const uint64_t tile_stride = (uint64_t)gridDim.x * WARPS;
   // mirror mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
+  auto block_of = [&](uint64_t tl) { return (tl << TB) >> 4; };
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
-      while (tl < n_tiles && (tl >> 1) > pair_swap(tl >> 1)) tl += (uint64_t)gridDim.x * WARPS;
+      while (tl < n_tiles && block_of(tl) > pair_swap(block_of(tl))) tl += tile_stride;
     return tl;
   };
   uint64_t tile = next_tile((uint64_t)blockIdx.x * WARPS + warp);
   double2* const wbuf = sX + warp * NBUF * 512;  // NBUF 512-double2 tiles (no indexed array:
                                                   // a dynamically indexed pointer array spills)
-  // element (lane, i): tuple t = tm & 7, member m = tm >> 3, address base(tile*8) + off
+  // element (lane, i): tuple t, member m, address base(tile*T) + off
   auto elem = [&](int i, int& t, int& m, uint64_t& off) {
     const int tm = lane_tm | sIterTM[i];
-    t = tm & 7;
-    m = tm >> 3;
+    t = tm & (T - 1);
+    m = tm >> TB;
     off = lane_off + sIterOff[i];
   };
   auto issue_load = [&](uint64_t tl, double2* buf) {
-    const double2* src = a + insert_zeros(tl * 8, p.lo_mask, 6);
+    const double2* src = a + insert_zeros(tl << TB, p.lo_mask, MB);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       int t, m;
       uint64_t off;
       elem(i, t, m, off);
-      const bool ok = tl * 8 + t < p.n_tuples;
-      cp_async16(buf + xs_idx(m, t), ok ? src + off : a, ok);
+      const bool ok = (tl << TB) + t < p.n_tuples;
+      cp_async16(buf + xs_idx<T>(m, t), ok ? src + off : a, ok);
     }
     cp_async_commit();
   };
@@ -574,29 +598,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       const GroupSub& g = sSub[s];
       const double2* F = sProg + g.s_off;
       if (g.k == 2) {
-        group_sub_k2<UI>(X, F, g.mi, g.mu, lane);
+        group_sub_k2<T, UI>(X, F, g.mi, g.mu, lane);
       } else if (g.k == 3) {
-        if constexpr (HAS3) group_sub_k3(X, F, lane);
+        if constexpr (HAS3 && NQ == 3) group_sub_k3(X, F, lane);
       } else {
-        group_sub_k1(X, F, g.mi, g.mu, lane);
+        group_sub_k1<T>(X, F, g.mi, g.mu, lane);
       }
       __syncwarp();
     }
     {
-      double2* dst = a + insert_zeros(tile * 8, p.lo_mask, 6);
+      double2* dst = a + insert_zeros(tile << TB, p.lo_mask, MB);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         int t, m;
         uint64_t off;
         elem(i, t, m, off);
-        if (tile * 8 + t < p.n_tuples) dst[off] = X[xs_idx(m, t)];
+        if ((tile << TB) + t < p.n_tuples) dst[off] = X[xs_idx<T>(m, t)];
       }
-      if (p.mirror && (tile >> 1) != pair_swap(tile >> 1)) {  // conj to transpose positions
-        double2* dstm = a + insert_zeros(pair_swap(tile * 8), p.lo_mask, 6);
+      if (p.mirror && block_of(tile) != pair_swap(block_of(tile))) {  // conj to transposes
+        double2* dstm = a + insert_zeros(pair_swap(tile << TB), p.lo_mask, MB);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int tm = mlane_tm | sIterTM[16 + i];
-          dstm[mlane_off + sIterOff[16 + i]] = cj(X[xs_idx(tm >> 3, tm & 7)]);
+          dstm[mlane_off + sIterOff[16 + i]] = cj(X[xs_idx<T>(tm >> TB, tm & (T - 1))]);
         }
       }
     }
@@ -605,13 +629,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-template <int WARPS, int NBUF, bool HAS3, int UI, int PMAX = kGroupProgMax>
-static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
+template <int NQ, int WARPS, int NBUF, bool HAS3, int UI, int PMAX = kGroupProgMax>
+static cudaError_t launch_group_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
   static bool attr_set = false;
+  constexpr int T = 1 << (9 - 2 * NQ);
   const size_t smem = (size_t)PMAX * sizeof(double2) +
                       (size_t)WARPS * NBUF * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
                       (size_t)kMaxSub * sizeof(GroupSub);
-  auto kern = group3_kernel<WARPS, NBUF, HAS3, UI, PMAX>;
+  auto kern = group_kernel<NQ, WARPS, NBUF, HAS3, UI, PMAX>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -620,7 +645,7 @@ static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStrea
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t tiles = (p.n_tuples + 7) / 8;
+  const uint64_t tiles = (p.n_tuples + T - 1) / T;
   const uint64_t ctas = (tiles + WARPS - 1) / WARPS;
   unsigned grid = (unsigned)(ctas < (uint64_t)sms ? ctas : (uint64_t)sms);
   if (grid < 1) grid = 1;
@@ -629,19 +654,11 @@ static cudaError_t launch_group3_cfg(double2* a, const GroupParams& p, cudaStrea
 }
 
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
+  if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);
   bool has3 = false;
   for (int i = 0; i < p.n_sub; ++i) has3 |= p.sub[i].k == 3;
-  if (has3) return launch_group3_cfg<8, 2, true, 4>(a, p, st);
-  static int cfg = -1;  // TANQ_G3=a|b|c|d selects the factored-group configuration
-  if (cfg < 0) {
-    const char* e = getenv("TANQ_G3");
-    cfg = e ? (e[0] - 'a') : 1;
-  }
-  if (cfg == 0) return launch_group3_cfg<8, 2, false, 4>(a, p, st);
-  if (cfg == 2) return launch_group3_cfg<16, 1, false, 1>(a, p, st);
-  if (cfg == 3 && p.prog_elems <= 2048)  // small programs: 12 warps, cp.async double buffer
-    return launch_group3_cfg<12, 2, false, 2, 2048>(a, p, st);
-  return launch_group3_cfg<16, 1, false, 2>(a, p, st);
+  if (has3) return launch_group_cfg<3, 8, 2, true, 4>(a, p, st);
+  return launch_group_cfg<3, 16, 1, false, 2>(a, p, st);
 }
 
 // ------------------------------------------------------------------------------------

@@ -65,13 +65,14 @@ class tanq_run_opts(ctypes.Structure):
 
 class tanq_run_stats(ctypes.Structure):
     _fields_ = [("ops_in", ctypes.c_uint64), ("ops_fused", ctypes.c_uint64),
-                ("gate_updates", ctypes.c_uint64), ("n_k", ctypes.c_uint64 * 4), ("n_remaps", ctypes.c_uint64),
+                ("gate_updates", ctypes.c_uint64), ("n_k", ctypes.c_uint64 * 5), ("n_remaps", ctypes.c_uint64),
                 ("remap_bytes", ctypes.c_uint64), ("plan_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {"ops_in": self.ops_in, "ops_fused": self.ops_fused,
                 "gate_updates": self.gate_updates,
                 "n_k1": self.n_k[1], "n_k2": self.n_k[2], "n_k3": self.n_k[3],
+                "n_k4": self.n_k[4],
                 "n_remaps": self.n_remaps, "remap_bytes": self.remap_bytes,
                 "plan_ms": self.plan_ms}
 
@@ -234,7 +235,7 @@ class Plan:
     sim=None plans on the host only (tanq_plan_create_host) for an n-qubit register split
     over world_size shards."""
 
-    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
+    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=4, profile=False,
                  world_size: int = 1, graph: bool = False, mirror: bool = True):
         cc = CCircuit(circuit.ops)
         cn = CNoise(noise) if noise is not None else None
@@ -278,7 +279,7 @@ class Plan:
         out = []
         for i in range(self.info()["ops_fused"]):
             k = ctypes.c_int()
-            q = (ctypes.c_int * 3)()
+            q = (ctypes.c_int * 4)()
             _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, None), "tanq_plan_get_op")
             S = np.empty((4 ** k.value, 4 ** k.value), dtype=np.complex128)
             _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, S.ctypes.data),
@@ -433,7 +434,7 @@ class Simulator:
         _check(lib().tanq_apply_superop(self.h, len(q), q.ctypes.data, m.ctypes.data),
                "tanq_apply_superop")
 
-    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
+    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 4,
                     profile: bool = False, prepared=None, mirror: bool = True) -> dict:
         if isinstance(circuit, QasmCircuit):
             class _C:  # the library-owned op array
@@ -449,7 +450,7 @@ class Simulator:
                                       ctypes.byref(opts), ctypes.byref(st)), "tanq_run_circuit")
         return st.as_dict()
 
-    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
+    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 4,
              profile: bool = False, graph: bool = False, mirror: bool = True) -> "Plan":
         return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile, graph=graph,
                     mirror=mirror)

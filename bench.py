@@ -370,7 +370,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--fuse", type=int, default=2)
-    ap.add_argument("--kmax", type=int, default=4)
+    ap.add_argument("--kmax", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1,

@@ -126,7 +126,8 @@ typedef struct {
 /* fuse: 0 none, 1 paper (same qubit / same ordered pair), 2 greedy up to k_max
  * with the B200 cost model (default).  k_max in {1,2,3,4}: fused superoperators never exceed
  * 2 qubits (or a user's 3-qubit op); k_max >= 3 lets the K3 group kernel run several of them
- * in one HBM pass over 3-qubit (k_max = 3) or up to 4-qubit tiles (k_max = 4, default).  chunk_bytes: remap staging chunk
+ * in one HBM pass over 3-qubit (k_max = 3, default) or up to 4-qubit tiles (k_max = 4; slower
+ * at n = 16 on B200).  chunk_bytes: remap staging chunk
  * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
  * on single-shard handles capture their launches into a CUDA graph on the first
  * tanq_plan_exec and replay it afterwards (ignored with bit0); bit2 = disable the

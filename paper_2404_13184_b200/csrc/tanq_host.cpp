@@ -1593,7 +1593,7 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   if (!c || !out) return fail(TANQ_E_ARG, "NULL argument");
   *out = nullptr;
   if (c->n_ops && !c->ops) return fail(TANQ_E_ARG, "ops is NULL");
-  tanq_run_opts opts{2, 4, 0, 0, 0};
+  tanq_run_opts opts{2, 3, 0, 0, 0};
   if (o) opts = *o;
   if (opts.fuse < 0 || opts.fuse > 2) return fail(TANQ_E_ARG, "fuse must be 0, 1 or 2");
   if (opts.k_max < 1 || opts.k_max > 4) return fail(TANQ_E_ARG, "k_max must be 1..4");

@@ -235,7 +235,7 @@ class Plan:
     sim=None plans on the host only (tanq_plan_create_host) for an n-qubit register split
     over world_size shards."""
 
-    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=4, profile=False,
+    def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
                  world_size: int = 1, graph: bool = False, mirror: bool = True):
         cc = CCircuit(circuit.ops)
         cn = CNoise(noise) if noise is not None else None
@@ -434,7 +434,7 @@ class Simulator:
         _check(lib().tanq_apply_superop(self.h, len(q), q.ctypes.data, m.ctypes.data),
                "tanq_apply_superop")
 
-    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 4,
+    def run_circuit(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
                     profile: bool = False, prepared=None, mirror: bool = True) -> dict:
         if isinstance(circuit, QasmCircuit):
             class _C:  # the library-owned op array
@@ -450,7 +450,7 @@ class Simulator:
                                       ctypes.byref(opts), ctypes.byref(st)), "tanq_run_circuit")
         return st.as_dict()
 
-    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 4,
+    def plan(self, circuit, noise=None, *, fuse: int = 2, k_max: int = 3,
              profile: bool = False, graph: bool = False, mirror: bool = True) -> "Plan":
         return Plan(self, circuit, noise, fuse=fuse, k_max=k_max, profile=profile, graph=graph,
                     mirror=mirror)

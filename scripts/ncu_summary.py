@@ -47,7 +47,7 @@ def main():
     ap.add_argument("--n", type=int, required=True, help="qubits of the captured run (alg bytes = 32*4^n)")
     ap.add_argument("--bytes-per-amp", type=float, default=32.0,
                     help="algorithmic bytes per amplitude of the captured launches (24 in mirror mode)")
-    ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,group3=group_k3_dmma")
+    ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,group_kernel=group_dmma")
     args = ap.parse_args()
     nmap = [kv.split("=") for kv in args.name_map.split(",")]
     traffic = json.load(open(args.traffic)) if os.path.exists(args.traffic) else {}

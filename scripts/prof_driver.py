@@ -14,7 +14,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--n", type=int, default=14)
     ap.add_argument("--depth", type=int, default=None)
-    ap.add_argument("--kmax", type=int, default=2)
+    ap.add_argument("--kmax", type=int, default=3)
     ap.add_argument("--reps", type=int, default=1)
     args = ap.parse_args()
     import workloads as W

@@ -214,6 +214,8 @@ def run_ours(args):
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         sim = Simulator(n, world_size=world, rank=rank, device=local, nccl_uid=uid[0])
+    elif "WORLD_SIZE" in os.environ and args.shards == 1:  # torchrun N=1: the per-rank API
+        sim = Simulator(n, world_size=1, rank=0, device=local)
     else:
         sim = Simulator(n, args.shards)
     stream = torch.cuda.Stream()          # a real stream: events on it bracket the kernels

@@ -401,3 +401,12 @@ def test_mirror_mode_state_tracking(Sim):
         c2 = W.Circuit(n, c.ops[:20] + [W.Op("superop", (1, 4), mat=S)] + c.ops[20:])
         sim.run_circuit(c2, nm)
         assert_parity(rho_of(sim, n), dense.run(c2, nm))
+
+
+def test_dist_handle_world1(Sim):
+    """tanq_create_dist with world_size 1 (the torchrun N=1 path) matches the oracle."""
+    c, nm = W.config_workload(4, n=6)
+    with Sim(6, world_size=1, rank=0, device=0) as sim:
+        sim.run_circuit(c, nm)
+        assert_parity(rho_of(sim, 6), dense.run(c, nm))
+        assert sim.info()["world_size"] == 1

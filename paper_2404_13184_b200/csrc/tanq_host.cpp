@@ -1172,12 +1172,16 @@ tanq_status combine_probs(tanq_sim* s, DevScratch*& primary) {
     NCCL_TRY(nccl().AllReduce(primary->imax, primary->imax, 1, ncclUint64, ncclMax, s->comm,
                               s0.stream));
   }
-  // |Im diag| check
+  // |Im diag| check (stream-ordered read: the library streams are non-blocking)
   double imx = 0.0;
   for (DevScratch* d : devs) {
     unsigned long long bits = 0;
+    cudaStream_t st = s0.stream;
+    for (auto& sh : s->shards)
+      if (sh.device == d->device) st = sh.stream;
     CUDA_TRY(cudaSetDevice(d->device));
-    CUDA_TRY(cudaMemcpy(&bits, d->imax, sizeof(bits), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(&bits, d->imax, sizeof(bits), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     double v;
     std::memcpy(&v, &bits, sizeof(v));
     imx = std::max(imx, v);
@@ -1565,7 +1569,10 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
       if (st != TANQ_OK) break;
     }
     cudaError_t ce = cudaStreamEndCapture(sh.stream, &graph);
-    if (st != TANQ_OK) return st;
+    if (st != TANQ_OK) {
+      if (ce == cudaSuccess) cudaGraphDestroy(graph);
+      return st;
+    }
     if (ce != cudaSuccess) return fail(TANQ_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
     ce = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -1931,6 +1938,7 @@ static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c6
                                          first + off, cnt, false, sh.stream));
         s->launches++;
       }
+      for (auto& sh : s->shards) TRY(stream_wait(s0, sh));  // every shard's gather lands first
       CUDA_TRY(cudaMemcpyAsync(out + off, d.stage, cnt * sizeof(double2), cudaMemcpyDeviceToHost,
                                s0.stream));
       CUDA_TRY(cudaStreamSynchronize(s0.stream));

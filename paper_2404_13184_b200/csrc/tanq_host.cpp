@@ -284,14 +284,15 @@ struct FusedOp {
   std::vector<FusedOp> sub;  // k=3 factored group: sub-ops applied in order in one pass
 };
 
-// B200 cost model in units of one HBM read+write pass (32 B / amplitude), DESIGN.md §6,
-// calibrated with scripts/kbench.py on B200 (n=14, profiles/r01_kbench_*): K1 ~6.8 TB/s
-// (1 pass), K2 5.0-6.5 TB/s (~1.15), a dense k=3 op on DMMA ~3.08 passes (FP64 bound).  A
-// factored K3 group costs 0.24 + its sub-ops' FP64 time: k=1 0.10, k=2 0.66 passes.
-double sep_cost(int k) { return k == 1 ? 1.0 : (k == 2 ? 1.15 : 3.08); }
-double sub_cost(int k) { return k == 1 ? 0.10 : (k == 2 ? 0.66 : 3.08); }
-constexpr double kGroupBase = 0.24;
-double op_cost(int k) { return k <= 2 ? 1.0 : 3.08; }
+// B200 cost model in units of one K1 pass over the state (mirror mode: 24 B / amplitude),
+// DESIGN.md §6, calibrated with scripts/kbench.py at n = 16 on B200 (profiles/r01_kbench_n16*):
+// K1 16.4 ms = 1, K2 17.1-17.5 ms (~1.05; high targets on cooperative tiles), a dense k=3 op on
+// DMMA 34.8 ms (2.12, FP64 bound).  A factored group costs 0.45 + its sub-ops' FP64 time:
+// 0.38 per k=2 sub-op (2 ops 1.21-1.34, 3 ops 1.55-1.75, 4 ops 1.96-1.98), k=1 ~0.06.
+double sep_cost(int k) { return k == 1 ? 1.0 : (k == 2 ? 1.05 : 2.12); }
+double sub_cost(int k) { return k == 1 ? 0.06 : (k == 2 ? 0.38 : 2.12); }
+constexpr double kGroupBase = 0.45;
+double op_cost(int k) { return k <= 2 ? 1.0 : 2.12; }
 
 bool shares(const FusedOp& a, const int* q, int k) {
   for (int i = 0; i < a.k; ++i)
@@ -398,6 +399,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
           if (uk >= lim) fits = false; else uq[uk++] = G.q[j];
         }
       }
+      if (uk > lim) fits = false;  // a dense k=3 op never joins a 4-qubit group
       if (fits) {
         Q.op.k = uk;
         for (int i = 0; i < uk; ++i) Q.op.q[i] = uq[i];
@@ -799,8 +801,29 @@ bool use_mirror(const tanq_sim* s, const FusedOp& op) {
   return op.k == 1 ? tuple_bits >= 2 : tuple_bits >= 4;
 }
 
+// k = 2 ops whose targets all sit at physical position >= 6 run as 2-qubit cooperative tiles
+// (tile_kernel<2>: 512 B contiguous copies); the register-streaming gate2_mma_kernel reads
+// 8 tuples = 128 B runs per member there (microbench/locality.cu).  Env TANQ_K2PATH =
+// direct | tile | auto (default).
+bool k2_tiled(const tanq_sim* s, const FusedOp& op) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("TANQ_K2PATH");
+    mode = e && !std::strcmp(e, "direct") ? 0 : (e && !std::strcmp(e, "tile") ? 1 : 2);
+  }
+  if (op.k != 2 || mode == 0) return false;
+  if (mode == 1) return true;
+  int lo = 64;
+  for (int j = 0; j < 2; ++j)
+    lo = std::min(lo, (int)std::min(s->phys[2 * op.q[j]], s->phys[2 * op.q[j] + 1]));
+  return lo >= 6;
+}
+
+// ops launched through the group / tile program path
+bool uses_prog(const tanq_sim* s, const FusedOp& op) { return op.k >= 3 || k2_tiled(s, op); }
+
 size_t group_prog_elems(const FusedOp& op) {
-  if (op.sub.empty()) return tanq::group_frag_elems(3);
+  if (op.sub.empty()) return tanq::group_frag_elems(op.k);
   size_t e = 0;
   for (const auto& sb : op.sub) e += tanq::group_frag_elems(sb.k);
   return e;
@@ -809,7 +832,7 @@ size_t group_prog_elems(const FusedOp& op) {
 // Build the K3 group program (sub-op headers + fragment-ordered matrices) for the current
 // layout; returns the kernel parameters except `prog`.
 void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, double2* prog) {
-  const int TBITS = 2 * op.k;  // 6 (3-qubit tile) or 8 (4-qubit tile)
+  const int TBITS = 2 * op.k;  // 4, 6 or 8 (2-, 3- or 4-qubit tile)
   const MemberMap tile = member_map(s, op.k, op.q);
   p.nq = op.k;
   for (int t = 0; t < 8; ++t) {
@@ -872,7 +895,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   const double amps = (double)((uint64_t)1 << s->L);
   // algorithmic: 8 flops per complex MAC; executed: K1 (FMA) 8, K2 / K3 (3-multiply DMMA) 6
   double flops_amp = 8.0 * M, hw_amp = (k == 1 ? 8.0 : 6.0) * M;
-  if (k >= 3 && !op.sub.empty()) {
+  if (gp && !op.sub.empty()) {
     flops_amp = hw_amp = 0;
     for (const auto& sb : op.sub) {
       const int Ms = 1 << (2 * sb.k);
@@ -882,19 +905,26 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   }
   MemberMap mm;
   std::vector<double2> Sm;
-  if (k < 3) {
+  if (!gp) {
     mm = member_map(s, k, op.q);
     Sm = member_order_S(op, mm);
   }
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
     // mirror mode reads only the canonical half of the tuples: 24 B / amplitude, half the flops
-    const bool mir = k < 3 ? use_mirror(s, op) : gp->mirror != 0;  // groups: k = 3 or 4
+    const bool mir = gp ? gp->mirror != 0 : use_mirror(s, op);
     const double fr = mir ? 0.5 : 1.0;
     Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 24.0 : 32.0) * amps,
             fr * flops_amp * amps, fr * hw_amp * amps};
     prof_begin(s, sh, pr);
-    if (k == 1) {
+    if (gp) {
+      int di = 0;
+      for (size_t i = 0; i < s->scratch.size(); ++i)
+        if (s->scratch[i].device == sh.device) di = (int)i;
+      tanq::GroupParams p = *gp;
+      p.prog = (*prog)[di];
+      CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
+    } else if (k == 1) {
       tanq::GateParams<1> p;
       std::memcpy(p.S, Sm.data(), sizeof(p.S));
       for (int t = 0; t < 2; ++t) {
@@ -915,12 +945,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       p.mirror = mir ? 1u : 0u;
       CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
     } else {
-      int di = 0;
-      for (size_t i = 0; i < s->scratch.size(); ++i)
-        if (s->scratch[i].device == sh.device) di = (int)i;
-      tanq::GroupParams p = *gp;
-      p.prog = (*prog)[di];
-      CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
+      return fail(TANQ_E_UNSUPPORTED, "k >= 3 op without a group program");
     }
     s->launches++;
     prof_end(s, sh, pr);
@@ -944,7 +969,7 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   // into a persistent pinned host buffer and copied (async) to each device before the launch.
   size_t total = 0;
   for (const auto& op : ops)
-    if (op.k >= 3) total += group_prog_elems(op);
+    if (op.k >= 2) total += group_prog_elems(op);  // k = 2: tiled or not, decided at launch
   if (total) {
     for (auto& sh : s->shards) {
       DevScratch& d = scratch_for(s, sh.device);
@@ -966,7 +991,7 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   for (size_t i = 0; i < ops.size(); ++i) {
     const FusedOp& op = ops[i];
     TRY(ensure_local(s, op, &ops, i + 1));
-    if (op.k < 3) {
+    if (!uses_prog(s, op)) {
       TRY(launch_op(s, op, nullptr, nullptr));
       continue;
     }
@@ -1532,12 +1557,12 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     }
     size_t total = 0;
     for (const auto& op : p->ops)
-      if (op.k >= 3) total += group_prog_elems(op);
+      if (uses_prog(s, op)) total += group_prog_elems(op);
     std::vector<double2> host(total ? total : 1);
     std::vector<tanq::GroupParams> gps;
     size_t off = 0;
     for (const auto& op : p->ops)
-      if (op.k >= 3) {
+      if (uses_prog(s, op)) {
         gps.emplace_back();
         build_group(s, op, gps.back(), host.data() + off);
         off += gps.back().prog_elems;
@@ -1559,7 +1584,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     size_t gi = 0;
     tanq_status st = TANQ_OK;
     for (const auto& op : p->ops) {
-      if (op.k < 3) {
+      if (!uses_prog(s, op)) {
         st = launch_op(s, op, nullptr, nullptr);
       } else {
         ptr[di] = g.dprog + off;

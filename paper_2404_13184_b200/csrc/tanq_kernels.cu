@@ -328,7 +328,10 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
 template <int T>
 __device__ __forceinline__ int xs_idx(int m, int t) {
   const int e = m * T + t;
-  return e ^ ((e >> 3) & 7);
+  if constexpr (T == 32)  // 2-qubit tiles (32 tuples x 16 members): slot t ^ f(m), f = 0,3,4,7
+    return e ^ (((m & 3) << 1) | (m & 1));
+  else
+    return e ^ ((e >> 3) & 7);
 }
 
 size_t group_frag_elems(int k) { return k == 3 ? 4096 : (k == 2 ? 256 : 16); }
@@ -377,7 +380,7 @@ __device__ __forceinline__ void group_sub_k3(double2* X, const double2* F, int l
 template <int T, int UI>  // T tuples per tile; UI n-tiles (of 8 columns) processed at once
 __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const uint8_t* mi,
                                              const uint8_t* mu, int lane) {
-  constexpr int TB = T == 8 ? 3 : 1;
+  constexpr int TB = T == 32 ? 5 : (T == 8 ? 3 : 1);
   const int r4 = lane >> 2, c4 = lane & 3;
   double sr[2][4], si[2][4], ss[2][4];
 #pragma unroll
@@ -449,7 +452,7 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
 template <int T>
 __device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const uint8_t* mi,
                                              const uint8_t* mu, int lane) {
-  constexpr int TB = T == 8 ? 3 : 1;
+  constexpr int TB = T == 32 ? 5 : (T == 8 ? 3 : 1);
   double2 S[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) S[i] = F[i];
@@ -653,12 +656,227 @@ static cudaError_t launch_group_cfg(double2* a, const GroupParams& p, cudaStream
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------
+// Cooperative tiles: one CTA (WARPS warps) owns a tile of WARPS x 512 amplitudes = TT tuples x
+// 4^NQ members (TT = WARPS x T; 4 warps: 128 tuples for NQ = 2, 32 for NQ = 3, 8 for NQ = 4).
+// The tile's index bits -- the TTB lowest free physical positions (tuple bits) and the 2 NQ
+// member positions -- include physical positions 0..4 whenever TTB >= 5, so every warp-wide
+// copy instruction moves one contiguous 512 B run (microbench/locality.cu: 5.9-6.1 TB/s for
+// any member positions, against 4.1-4.9 TB/s for 8-tuple warp tiles whose members sit at
+// position >= 6).  Warp w computes on tuples [wT, (w+1)T) of the tile with the sub-op code
+// above; only the copies are shared.
+// Mirror mode: canonical unit = block of 2^BB tiles (BB = TTB & 1, so the block index starts
+// at an even tuple bit); a block is processed when block <= pair_swap(block), and writes
+// conjugates to the transposed block unless it is its own transpose.
+// ------------------------------------------------------------------------------------
+template <int NQ, int WARPS, int NBUF, int UI>
+__global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
+    tile_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
+  constexpr int MB = 2 * NQ, TB = 9 - MB, T = 1 << TB;
+  constexpr int WB = WARPS == 8 ? 3 : (WARPS == 4 ? 2 : 1), TTB = TB + WB, TT = 1 << TTB;
+  constexpr int HB = 5 + WB, NBITS = HB + 4, BB = TTB & 1, ELEMS = WARPS * 512;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // shared: program | NBUF tiles | copy tables [2][16] | sub-op headers
+  const int prog_cap = (p.prog_elems + 7) & ~7;
+  double2* sProg = reinterpret_cast<double2*>(smem_raw);
+  double2* sX = sProg + prog_cap;
+  uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + NBUF * ELEMS);
+  int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);
+  GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int freep[TTB + 1];
+  {
+    int nf = 0;
+    for (int f = 0; f < 64 && nf < TTB + 1; ++f) {
+      bool tgt = false;
+      for (int j = 0; j < MB; ++j) tgt |= (int)p.pos[j] == f;
+      if (!tgt) freep[nf++] = f;
+    }
+  }
+  // NBITS tile bits sorted by physical position: threads take the HB lowest, iterations the
+  // next 4.  Mirror map: tuple bit j lands on freep[j^1], member bit j on pos[j^1].
+  auto build_map = [&](bool mir, int& ttm, uint64_t& toff, int* it_tm, uint64_t* it_off) {
+    int bit_pos[NBITS], bit_id[NBITS];  // id < TTB: tuple bit, else member bit id-TTB
+    for (int j = 0; j < TTB; ++j) {
+      bit_pos[j] = freep[mir ? (j ^ 1) : j];
+      bit_id[j] = j;
+    }
+    for (int j = 0; j < MB; ++j) {
+      bit_pos[TTB + j] = (int)p.pos[mir ? (j ^ 1) : j];
+      bit_id[TTB + j] = TTB + j;
+    }
+    for (int x = 1; x < NBITS; ++x)
+      for (int y = x; y > 0 && bit_pos[y] < bit_pos[y - 1]; --y) {
+        int tp = bit_pos[y]; bit_pos[y] = bit_pos[y - 1]; bit_pos[y - 1] = tp;
+        int ti = bit_id[y]; bit_id[y] = bit_id[y - 1]; bit_id[y - 1] = ti;
+      }
+    auto tm_of = [&](int bits, int first, int cnt, uint64_t& off) {
+      int t = 0, m = 0;
+      off = 0;
+      for (int b = 0; b < cnt; ++b)
+        if ((bits >> b) & 1) {
+          const int id = bit_id[first + b];
+          if (id < TTB) t |= 1 << id; else m |= 1 << (id - TTB);
+          off += (uint64_t)1 << bit_pos[first + b];
+        }
+      return t | (m << TTB);
+    };
+    ttm = tm_of(threadIdx.x, 0, HB, toff);
+    if (threadIdx.x < 16) it_tm[threadIdx.x] = tm_of(threadIdx.x, HB, 4, it_off[threadIdx.x]);
+  };
+  int thr_tm, mthr_tm = 0;
+  uint64_t thr_off, mthr_off = 0;
+  build_map(false, thr_tm, thr_off, sIterTM, sIterOff);
+  if (p.mirror) build_map(true, mthr_tm, mthr_off, sIterTM + 16, sIterOff + 16);
+  for (int e = threadIdx.x; e < p.prog_elems; e += blockDim.x) sProg[e] = p.prog[e];
+  for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
+  __syncthreads();
+
+  const uint64_t n_tiles = (p.n_tuples + TT - 1) >> TTB;
+  auto next_tile = [&](uint64_t tl) {
+    if (p.mirror)
+      while (tl < n_tiles && (tl >> BB) > pair_swap(tl >> BB)) tl += gridDim.x;
+    return tl;
+  };
+  // shared index of tile element (tuple t, member m): warp sub-tile t / T, swizzled inside
+  auto sidx = [](int tm) {
+    const int t = tm & (TT - 1), m = tm >> TTB;
+    return ((t >> TB) << 9) + xs_idx<T>(m, t & (T - 1));
+  };
+  auto issue_load = [&](uint64_t tl, double2* buf) {
+    const double2* src = a + insert_zeros(tl << TTB, p.lo_mask, MB) + thr_off;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int tm = thr_tm | sIterTM[i];
+      const bool ok = (tl << TTB) + (tm & (TT - 1)) < p.n_tuples;
+      cp_async16(buf + sidx(tm), ok ? src + sIterOff[i] : a, ok);
+    }
+    cp_async_commit();
+  };
+
+  // NBUF = 2: the next tile's copies are issued right after the barrier that makes the current
+  // tile visible, so they overlap the compute and the stores (2 barriers per tile).
+  uint64_t tile = next_tile(blockIdx.x);
+  if (NBUF == 2 && tile < n_tiles) issue_load(tile, sX);
+  int cur = 0;
+  while (tile < n_tiles) {
+    const uint64_t next = next_tile(tile + gridDim.x);
+    if constexpr (NBUF == 1) issue_load(tile, sX);
+    cp_async_wait<0>();
+    __syncthreads();  // current tile visible; the other buffer's stores are done
+    if constexpr (NBUF == 2)
+      if (next < n_tiles) issue_load(next, sX + (cur ^ 1) * ELEMS);
+    double2* buf = sX + (NBUF == 2 ? cur * ELEMS : 0);
+    double2* X = buf + (warp << 9);
+    for (int s = 0; s < p.n_sub; ++s) {
+      const GroupSub& g = sSub[s];
+      const double2* F = sProg + g.s_off;
+      if (g.k == 2)
+        group_sub_k2<T, UI>(X, F, g.mi, g.mu, lane);
+      else
+        group_sub_k1<T>(X, F, g.mi, g.mu, lane);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      double2* dst = a + insert_zeros(tile << TTB, p.lo_mask, MB) + thr_off;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int tm = thr_tm | sIterTM[i];
+        if ((tile << TTB) + (tm & (TT - 1)) < p.n_tuples) dst[sIterOff[i]] = buf[sidx(tm)];
+      }
+      const uint64_t blk = tile >> BB;
+      if (p.mirror && pair_swap(blk) != blk) {  // conjugates to the transposed block
+        double2* dstm = a + insert_zeros(pair_swap(tile << TTB), p.lo_mask, MB) + mthr_off;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          dstm[sIterOff[16 + i]] = cj(buf[sidx(mthr_tm | sIterTM[16 + i])]);
+      }
+    }
+    if constexpr (NBUF == 1) __syncthreads();  // the buffer is reloaded next
+    tile = next;
+    cur ^= 1;
+  }
+}
+
+static int g_tile_mode = -1;  // env TANQ_GROUP=warp: the per-warp group_kernel (comparison)
+
+template <int NQ, int WARPS, int NBUF, int UI>
+static cudaError_t launch_tile_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  constexpr int TT = WARPS << (9 - 2 * NQ);
+  const size_t smem = (size_t)((p.prog_elems + 7) & ~7) * sizeof(double2) +
+                      (size_t)NBUF * WARPS * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
+                      (size_t)p.n_sub * sizeof(GroupSub);
+  auto kern = tile_kernel<NQ, WARPS, NBUF, UI>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t tiles = (p.n_tuples + TT - 1) / TT;
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+  kern<<<grid, WARPS * 32, smem, st>>>(a, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
-  if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);
+  if (g_tile_mode < 0) {  // env TANQ_GROUP = auto | warp | q1 | q2 | p1 | p2 (experiments)
+    const char* e = getenv("TANQ_GROUP");
+    g_tile_mode = !e ? -2
+                     : !strcmp(e, "warp") ? 0
+                     : !strcmp(e, "q1")   ? 1
+                     : !strcmp(e, "q2")   ? 2
+                     : !strcmp(e, "p1")   ? 3
+                     : !strcmp(e, "p2")   ? 4 : -2;
+  }
   bool has3 = false;
   for (int i = 0; i < p.n_sub; ++i) has3 |= p.sub[i].k == 3;
+  // dense 64x64 sub-ops are DMMA-bound: per-warp tiles, 2 buffers, 8 independent warps
+  if (has3 && p.nq != 3) return cudaErrorInvalidValue;  // the planner never emits this
   if (has3) return launch_group_cfg<3, 8, 2, true, 4>(a, p, st);
-  return launch_group_cfg<3, 16, 1, false, 2>(a, p, st);
+  int mode = g_tile_mode;
+  if (mode == -2) {
+    // auto (measured at n = 16, scripts/kbench.py): cooperative tiles win while the group is
+    // memory-bound (<= 2 k=2 sub-ops) and its lowest member position is >= 6 (per-warp tiles
+    // then read 128 B runs, microbench/locality.cu); heavier programs are DMMA-bound and run
+    // best on 16 independent warps.
+    uint32_t lo = 64;
+    for (int j = 0; j < 2 * p.nq; ++j) lo = p.pos[j] < lo ? p.pos[j] : lo;
+    int n2 = 0;
+    for (int i = 0; i < p.n_sub; ++i) n2 += p.sub[i].k == 2;
+    mode = (p.nq == 2 || (lo > 5 && n2 <= 2)) ? 1 : 0;
+  }
+  if (p.nq == 2 && mode == 0) mode = 1;
+  switch (mode) {
+    case 0:
+      if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);
+      return launch_group_cfg<3, 16, 1, false, 2>(a, p, st);
+    case 2:
+      if (p.nq == 2) return launch_tile_cfg<2, 4, 2, 2>(a, p, st);
+      if (p.nq == 4) return launch_tile_cfg<4, 4, 2, 1>(a, p, st);
+      return launch_tile_cfg<3, 4, 2, 2>(a, p, st);
+    case 3:
+      if (p.nq == 2) return launch_tile_cfg<2, 2, 1, 2>(a, p, st);
+      if (p.nq == 4) return launch_tile_cfg<4, 2, 1, 1>(a, p, st);
+      return launch_tile_cfg<3, 2, 1, 2>(a, p, st);
+    case 4:
+      if (p.nq == 2) return launch_tile_cfg<2, 2, 2, 2>(a, p, st);
+      if (p.nq == 4) return launch_tile_cfg<4, 2, 2, 1>(a, p, st);
+      return launch_tile_cfg<3, 2, 2, 2>(a, p, st);
+    default:
+      if (p.nq == 2) return launch_tile_cfg<2, 4, 1, 2>(a, p, st);
+      if (p.nq == 4) return launch_tile_cfg<4, 4, 1, 1>(a, p, st);
+      return launch_tile_cfg<3, 4, 1, 2>(a, p, st);
+  }
 }
 
 // ------------------------------------------------------------------------------------

@@ -48,7 +48,8 @@ def main():
             print(json.dumps(out[-1]), flush=True)
         # K3 groups: chains of k=2 channels inside 3 qubits, one pass (fuse=2, k_max=3)
         groups = [[(0, 1), (1, 2)], [(1, 2), (2, 3), (1, 3)], [(5, n - 1), (n - 1, n - 2)],
-                  [(0, 1), (1, 2), (0, 2), (2, 1)], [(3, 7), (7, n - 1), (3, n - 1), (7, 3), (3, 7)]]
+                  [(0, 1), (1, 2), (0, 2), (2, 1)], [(3, 7), (7, n - 1), (3, n - 1), (7, 3), (3, 7)],
+                  [(8, 10), (10, 12), (8, 12)], [(n - 3, n - 2), (n - 2, n - 1), (n - 3, n - 1), (n - 2, n - 3)]]
         for g in groups:
             ops = [W.Op("kraus", qs, kraus=W.random_kraus(rng, 4, 2)) for qs in g]
             plan = sim.plan(W.Circuit(n, ops), None, fuse=2, k_max=3)

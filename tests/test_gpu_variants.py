@@ -1,0 +1,56 @@
+"""GPU parity of every group / k=2 kernel variant (-m gpu).
+
+The library picks a kernel per launch (per-warp tiles, cooperative 4- or 2-warp tiles with one
+or two buffers, direct or tiled k=2); the choice is read once per process from TANQ_GROUP /
+TANQ_K2PATH, so each forced variant runs in its own interpreter.  Every variant must match the
+CPU oracle at the north-star bar on random noisy circuits (groups of 3 and 4 qubits, mirror
+mode on and off, ragged small registers).
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SNIPPET = r"""
+import numpy as np, sys
+sys.path.insert(0, %(root)r)
+import workloads as W
+from oracle import dense
+from paper_2404_13184_b200 import Simulator
+worst = 0.0
+for seed in range(4):
+    n = 4 + seed                              # 4..7 qubits: one partial tile up to many tiles
+    c = W.random_circuit(n, 60, seed=4200 + seed, kmax=3)
+    nm = W.synthetic_calibration(c, seed, depol=True, thermal=True, overrot=True)
+    ref = dense.run(c, nm)
+    N = 2 ** n
+    for kmax in (3, 4):
+        for mirror in (True, False):
+            with Simulator(n) as sim:
+                sim.run_circuit(c, nm, fuse=2, k_max=kmax, mirror=mirror)
+                got = sim.get_state().reshape(N, N).T
+            d = got - ref
+            mx = np.abs(d).max()
+            rel = np.linalg.norm(d) / np.linalg.norm(ref)
+            assert mx <= 1e-10 and rel <= 1e-12, (seed, kmax, mirror, mx, rel)
+            worst = max(worst, mx)
+print("OK", worst)
+"""
+
+
+@pytest.mark.parametrize("group,k2path", [("warp", "direct"), ("q1", "tile"), ("q2", "tile"),
+                                          ("p1", "tile"), ("p2", "auto"), ("auto", "auto")])
+def test_kernel_variant_parity(group, k2path):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path)
+    r = subprocess.run([sys.executable, "-c", SNIPPET % {"root": ROOT}], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert r.stdout.strip().splitlines()[-1].startswith("OK")

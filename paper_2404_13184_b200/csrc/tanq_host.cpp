@@ -466,7 +466,8 @@ struct Prof {
   cudaEvent_t e0, e1;
   double bytes, flops, hw_flops;
 };
-const char* kProfNames[] = {"gate_k1", "gate_k2", "group_dmma", "remap"};
+constexpr int kProfClasses = 5;
+const char* kProfNames[kProfClasses] = {"gate_k1", "gate_k2", "group_dmma", "remap", "unpack"};
 
 }  // namespace
 
@@ -509,12 +510,13 @@ struct tanq_sim {
   std::vector<cudaEvent_t> event_pool;  // recycled timing events (no create per launch)
   bool herm_state = true;   // rho known Hermitian (create / reset; cleared by set_state and
                             // by non-Hermiticity-preserving ops; tanq_check_hermitian sets it)
-  bool mirror_allowed = true;  // env TANQ_MIRROR=0 disables the mirror mode
-  double prof_ms[4] = {0, 0, 0, 0};
-  double prof_bytes[4] = {0, 0, 0, 0};
-  double prof_flops[4] = {0, 0, 0, 0};
-  double prof_hw_flops[4] = {0, 0, 0, 0};
-  uint64_t prof_launches[4] = {0, 0, 0, 0};
+  bool mirror_allowed = true;  // env TANQ_MIRROR=0 disables the packed Hermitian mode
+  bool packed = false;      // packed Hermitian layout: only e >= pair_swap(e) is up to date
+  double prof_ms[kProfClasses] = {};
+  double prof_bytes[kProfClasses] = {};
+  double prof_flops[kProfClasses] = {};
+  double prof_hw_flops[kProfClasses] = {};
+  uint64_t prof_launches[kProfClasses] = {};
   uint64_t launches = 0;
   uint64_t remap_count = 0, remap_bytes = 0;
   std::vector<std::pair<int, cudaStream_t>> owned;  // library-created stream per device
@@ -610,7 +612,10 @@ void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
 }
 
 // Swap physical bit a (global, a >= L) with local bit b (A-6).
+tanq_status ensure_unpacked(tanq_sim* s);
+
 tanq_status remap_swap(tanq_sim* s, int a, int b) {
+  TRY(ensure_unpacked(s));  // (packed mode is single-shard only; kept for safety)
   const int L = s->L, gb = a - L;
   const uint64_t half = (uint64_t)1 << (L - 1);
   if (!s->dist) {
@@ -790,8 +795,9 @@ std::vector<double2> member_order_S(const FusedOp& op, const MemberMap& mm) {
   return out;
 }
 
-// Mirror mode: rho known Hermitian, op Hermiticity-preserving, one shard with
-// the initial interleaved layout (row/col bits of every qubit adjacent), whole 16-tuple blocks.
+// Packed Hermitian mode: rho known Hermitian, op Hermiticity-preserving, one
+// shard with the initial interleaved layout (row/col bits of every qubit adjacent, so the
+// transpose of element e is pair_swap(e)), whole 16-tuple blocks.
 bool use_mirror(const tanq_sim* s, const FusedOp& op) {
   if (!s->mirror_allowed || !s->herm_state || !op.herm || s->shards.size() != 1 || s->dist)
     return false;
@@ -841,6 +847,12 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
   }
   p.n_tuples = (uint64_t)1 << (s->L - TBITS);
   p.mirror = use_mirror(s, op) ? 1u : 0u;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = std::getenv("TANQ_DBG");
+    dbg = e ? std::atoi(e) : 0;
+  }
+  p.dbg = (uint32_t)dbg;
   std::vector<const FusedOp*> subs;
   if (op.sub.empty())
     subs.push_back(&op);
@@ -886,6 +898,21 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
   p.prog_elems = (int)off;
 }
 
+// Packed -> full layout (one pass), before anything that reads or writes elements the packed
+// layout does not keep up to date.
+tanq_status ensure_unpacked(tanq_sim* s) {
+  if (!s->packed) return TANQ_OK;
+  Shard& sh = s->shards[0];
+  CUDA_TRY(cudaSetDevice(sh.device));
+  Prof pr{4, nullptr, nullptr, 16.0 * (double)((uint64_t)1 << s->L), 0.0, 0.0};
+  prof_begin(s, sh, pr);
+  CUDA_TRY(tanq::launch_unpack(sh.data, s->L, sh.stream));
+  prof_end(s, sh, pr);
+  s->launches++;
+  s->packed = false;
+  return TANQ_OK;
+}
+
 // Launch one fused op on every shard (targets must be local).  For k >= 3 (groups), `prog`
 // holds the group program already copied to each device (indexed like s->scratch).
 tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* gp,
@@ -903,6 +930,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       hw_amp += (sb.k == 1 ? 8.0 : 6.0) * Ms;
     }
   }
+  const bool mir_op = gp ? gp->mirror != 0 : use_mirror(s, op);
+  if (!mir_op) TRY(ensure_unpacked(s));
   MemberMap mm;
   std::vector<double2> Sm;
   if (!gp) {
@@ -912,9 +941,9 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
     // mirror mode reads only the canonical half of the tuples: 24 B / amplitude, half the flops
-    const bool mir = gp ? gp->mirror != 0 : use_mirror(s, op);
+    const bool mir = mir_op;
     const double fr = mir ? 0.5 : 1.0;
-    Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 24.0 : 32.0) * amps,
+    Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 16.0 : 32.0) * amps,
             fr * flops_amp * amps, fr * hw_amp * amps};
     prof_begin(s, sh, pr);
     if (gp) {
@@ -950,6 +979,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
     s->launches++;
     prof_end(s, sh, pr);
   }
+  if (mir_op) s->packed = true;
   if (!op.herm) s->herm_state = false;
   return TANQ_OK;
 }
@@ -1419,6 +1449,7 @@ tanq_status tanq_reset(tanq_sim* s) {
   }
   reset_layout(s);
   s->herm_state = true;
+  s->packed = false;
   return TANQ_OK;
 }
 
@@ -1518,7 +1549,7 @@ struct tanq_plan {
     const tanq_sim* sim = nullptr;
     const double2* data = nullptr;
     uint32_t phys[64];
-    bool herm = false, mirror = false;
+    bool herm = false, mirror = false, packed = false, packed_end = false;
     cudaGraphExec_t exec = nullptr;
     double2* dprog = nullptr;
     int device = -1;
@@ -1541,7 +1572,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
   Shard& sh = s->shards[0];
   auto& g = p->g;
   const bool hit = g.exec && g.sim == s && g.data == sh.data && g.herm == s->herm_state &&
-                   g.mirror == s->mirror_allowed &&
+                   g.mirror == s->mirror_allowed && g.packed == s->packed &&
                    std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0;
   CUDA_TRY(cudaSetDevice(sh.device));
   if (!hit) {
@@ -1557,16 +1588,20 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     }
     size_t total = 0;
     for (const auto& op : p->ops)
-      if (uses_prog(s, op)) total += group_prog_elems(op);
+      if (op.k >= 2) total += group_prog_elems(op);  // upper bound (k = 2 may run direct)
     std::vector<double2> host(total ? total : 1);
     std::vector<tanq::GroupParams> gps;
     size_t off = 0;
-    for (const auto& op : p->ops)
+    const bool herm_in = s->herm_state;
+    for (const auto& op : p->ops) {  // the Hermitian flag as it will be when op runs
       if (uses_prog(s, op)) {
         gps.emplace_back();
         build_group(s, op, gps.back(), host.data() + off);
         off += gps.back().prog_elems;
       }
+      if (!op.herm) s->herm_state = false;
+    }
+    s->herm_state = herm_in;
     if (total) {
       CUDA_TRY(cudaMalloc(&g.dprog, total * sizeof(double2)));
       CUDA_TRY(cudaMemcpy(g.dprog, host.data(), total * sizeof(double2), cudaMemcpyHostToDevice));
@@ -1576,7 +1611,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     int di = 0;
     for (size_t i = 0; i < s->scratch.size(); ++i)
       if (s->scratch[i].device == sh.device) di = (int)i;
-    const bool herm0 = s->herm_state;
+    const bool herm0 = s->herm_state, packed0 = s->packed;
     cudaGraph_t graph;
     CUDA_TRY(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal));
     const uint64_t l0 = s->launches;
@@ -1607,11 +1642,14 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     g.sim = s;
     g.data = sh.data;
     g.herm = herm0;
+    g.packed = packed0;
+    g.packed_end = s->packed;
     g.mirror = s->mirror_allowed;
     std::memcpy(g.phys, s->phys, sizeof(g.phys));
   }
   CUDA_TRY(cudaGraphLaunch(g.exec, sh.stream));
   s->launches += g.kernels;
+  s->packed = g.packed_end;
   for (const auto& op : p->ops)
     if (!op.herm) s->herm_state = false;
   return TANQ_OK;
@@ -1807,6 +1845,7 @@ tanq_status tanq_expect_pauli(tanq_sim* s, uint64_t xm, uint64_t zm, double* out
   if (!s || !out_re) return fail(TANQ_E_ARG, "NULL argument");
   const uint64_t lim = s->n >= 64 ? ~0ull : ((1ull << s->n) - 1);
   if ((xm & ~lim) || (zm & ~lim)) return fail(TANQ_E_ARG, "Pauli mask outside the register");
+  if (xm) TRY(ensure_unpacked(s));  // X / Y factors read off-diagonal elements
   tanq::BitMap bm = bitmap_of(s);
   const int nb = tanq::expect_blocks(s->n);
   double re = 0.0, im = 0.0;
@@ -1974,11 +2013,13 @@ static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c6
 
 tanq_status tanq_get_state(tanq_sim* s, uint64_t first, uint64_t count, tanq_c64* out) {
   if (!s || (!out && count)) return fail(TANQ_E_ARG, "NULL argument");
+  TRY(ensure_unpacked(s));
   return state_io(s, first, count, out, nullptr);
 }
 
 tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const tanq_c64* in) {
   if (!s || (!in && count)) return fail(TANQ_E_ARG, "NULL argument");
+  TRY(ensure_unpacked(s));  // elements outside [first, first + count) must stay valid
   s->herm_state = false;  // unknown until tanq_check_hermitian
   return state_io(s, first, count, nullptr, in);
 }
@@ -1986,6 +2027,10 @@ tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const ta
 tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm) {
   if (!s || !is_herm) return fail(TANQ_E_ARG, "NULL argument");
   *is_herm = 0;
+  if (s->packed) {  // the packed layout stores one element per transpose pair: Hermitian
+    *is_herm = 1;
+    return TANQ_OK;
+  }
   if (s->shards.size() != 1 || s->dist) return TANQ_OK;  // transpose pairs span shards
   for (int i = 0; i < 2 * s->n; ++i)
     if (s->phys[i] != (uint32_t)i) return TANQ_OK;
@@ -2019,7 +2064,7 @@ tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* 
   if (!s || !n_out) return fail(TANQ_E_ARG, "NULL argument");
   TRY(prof_flush(s));
   int n = 0;
-  for (int c = 0; c < 4 && n < max; ++c) {
+  for (int c = 0; c < kProfClasses && n < max; ++c) {
     if (!s->prof_launches[c]) continue;
     tanq_kernel_prof& p = out[n++];
     std::memset(&p, 0, sizeof(p));
@@ -2037,7 +2082,7 @@ tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* 
 tanq_status tanq_profile_reset(tanq_sim* s) {
   if (!s) return fail(TANQ_E_ARG, "NULL handle");
   TRY(prof_flush(s));
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < kProfClasses; ++c) {
     s->prof_ms[c] = s->prof_bytes[c] = s->prof_flops[c] = s->prof_hw_flops[c] = 0;
     s->prof_launches[c] = 0;
   }

@@ -20,7 +20,7 @@ struct GateParams {
   uint64_t lo_mask[2 * K];   // (1 << pos[j]) - 1
   uint64_t n_tuples;         // 2^(L - 2K)
   uint32_t pos[2 * K];
-  uint32_t mirror;           // 1: Hermitian mirror mode
+  uint32_t mirror;           // 1: packed Hermitian mode
 };
 
 // K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 4^nq-member tuples (2 nq
@@ -42,7 +42,9 @@ struct GroupParams {
   uint64_t lo_mask[8];
   uint64_t n_tuples;
   uint32_t pos[8];
-  uint32_t mirror;           // 1: Hermitian mirror mode
+  uint32_t mirror;           // 1: packed Hermitian mode
+  uint32_t dbg;              // profiling experiments only (env TANQ_DBG): 1 skip sub-ops,
+                             // 2 skip HBM copies; 0 in production
   GroupSub sub[kMaxSub];
 };
 
@@ -55,6 +57,8 @@ struct BitMap {               // physical bit of each logical bit (row q -> 2q, 
 cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st);
 cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st);
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st);
+// packed Hermitian layout -> full layout (single shard, interleaved identity bit map)
+cudaError_t launch_unpack(double2* a, int L, cudaStream_t st);
 size_t group_frag_elems(int k);                               // double2 per sub-op matrix
 void group_make_frags(int k, const double2* S_member_order, double2* frag /*host*/);
 

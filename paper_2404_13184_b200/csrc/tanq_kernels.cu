@@ -46,6 +46,27 @@ __device__ __forceinline__ uint64_t pair_swap(uint64_t x) {
 }
 __device__ __forceinline__ double2 cj(double2 v) { return make_double2(v.x, -v.y); }
 
+// Packed Hermitian layout: of each transpose pair {e, pair_swap(e)} only the
+// element with e <= pair_swap(e) is kept up to date (diagonal-type elements e = pair_swap(e)
+// always); the other is recovered as conj of its transpose.  Kernels in packed mode read and
+// write one element per pair: 16 B per amplitude per pass instead of 32.  The kernels process
+// the tuple / tile t <= pair_swap(t) of each transpose pair, whose elements are then mostly
+// stored in place (no conjugation, no transposed addresses) -- the same orientation.
+__device__ __forceinline__ bool packed_stored(uint64_t e, uint64_t e_mirror) { return e <= e_mirror; }
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+// A tile whose base index has a differing (row, col) pair above every in-tile position `hi`
+// orders all its elements against their transposes the same way: when that pair makes the
+// base the stored one, every element is read and written in place (the common case for the
+// canonical tiles the kernels visit) and the per-element test is skipped.
+__device__ __forceinline__ bool packed_tile_direct(uint64_t base, int hi) {
+  const uint64_t d = (base ^ (base >> 1)) & 0x5555555555555555ull;
+  if (!d) return false;
+  const int hb = 63 - __clzll(d);
+  return hb > hi && packed_stored(base, pair_swap(base));
+}
+
 __device__ __forceinline__ void ld32(const double2* p, double2& a, double2& b) {
   asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
@@ -88,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.n_tuples; t += stride) {
     uint64_t tm = t;
-    if (p.mirror) {  // only the canonical tuple of each transpose pair is read and computed
+    if (p.mirror) {  // packed mode: only the canonical tuple of each transpose pair
       tm = pair_swap(t);
       if (tm < t) continue;
     }
@@ -99,7 +120,6 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
       basem = ((basem & ~p.lo_mask[j]) << 1) | (basem & p.lo_mask[j]);
     }
     double2* ptr = a + base;
-    double2* ptrm = a + basem;
     uint64_t off[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -110,7 +130,15 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
       off[i] = o;
     }
     double2 x[M];
-    if constexpr (PAIR) {
+    if (p.mirror) {  // member i lives at its own address if stored there, else at its transpose
+#pragma unroll
+      for (int i = 0; i < M; ++i) {  // one load per element: select the address first
+        const uint64_t e = base + off[i], em = basem + off[pswap_c(i)];
+        const bool in_place = packed_stored(e, em);
+        const double2 v = a[in_place ? e : em];
+        x[i] = in_place ? v : cj(v);
+      }
+    } else if constexpr (PAIR) {
 #pragma unroll
       for (int i = 0; i < M; i += 2) ld32(ptr + off[i], x[i], x[i + 1]);
     } else {
@@ -133,15 +161,18 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
         }
         y[u] = make_double2(yr, yi);
       }
-      if constexpr (PAIR) {
+      if (p.mirror) {  // store each result where the packed layout keeps it
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint64_t e = base + off[l + u], em = basem + off[pswap_c(l + u)];
+          if (packed_stored(e, em)) a[e] = y[u];
+          else if (tm != t) a[em] = cj(y[u]);  // self tuple: the transpose is stored above
+        }
+      } else if constexpr (PAIR) {
         st32(ptr + off[l], y[0], y[1]);
       } else {
         ptr[off[l]] = y[0];
         ptr[off[l + 1]] = y[1];
-      }
-      if (tm != t) {  // transpose tuple: conj, member bit pairs swapped
-        ptrm[off[pswap_c(l)]] = cj(y[0]);
-        ptrm[off[pswap_c(l + 1)]] = cj(y[1]);
       }
     }
   }
@@ -156,9 +187,8 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
 //   D fragment = member 8mt + (lane>>2) of tuples 2(lane&3), 2(lane&3)+1 -> one 32 B store
 //   when consecutive tuples are adjacent in memory (physical bit 0 not a target).
 // The next tile's loads are issued before the current tile's DMMAs (register prefetch).
-// Mirror mode (Hermitian rho, Hermiticity-preserving S): only canonical 16-tuple blocks are
-// read and computed; every result is also written, conjugated, to its transpose position.
-// ------------------------------------------------------------------------------------
+// Packed Hermitian mode: canonical 16-tuple blocks only; each element is read from / written
+// to where the packed layout keeps it (self-transposed blocks: named barrier, in-place only).
 template <bool ADJ>
 __global__ void __launch_bounds__(256, 2)
     gate2_mma_kernel(double2* __restrict__ a, const __grid_constant__ GateParams<2> p) {
@@ -168,12 +198,17 @@ __global__ void __launch_bounds__(256, 2)
   const uint64_t n_tiles = (p.n_tuples + 7) >> 3;
   const int r4 = lane >> 2, c4 = lane & 3;
 
+  // S staged in shared memory: if register pressure makes the compiler re-load a fragment
+  // inside the loop it is a conflict-free LDS, not a lane-indexed (serialised) constant load
+  __shared__ double2 sS[256];
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) sS[e] = p.S[e];
+  __syncthreads();
   double sr[2][4], si[2][4], ss[2][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      const double2 v = p.S[(8 * mt + r4) * 16 + 4 * ks + c4];
+      const double2 v = sS[(8 * mt + r4) * 16 + 4 * ks + c4];
       sr[mt][ks] = v.x;
       si[mt][ks] = v.y;
       ss[mt][ks] = v.x + v.y;
@@ -185,8 +220,8 @@ __global__ void __launch_bounds__(256, 2)
       if ((m >> j) & 1) o += (uint64_t)1 << p.pos[j];
     return o;
   };
-  uint64_t offB[4], offD[2];
-#pragma unroll
+  uint64_t offB[4], offD[2];  // (transposed offsets are formed on the packed slow path only,
+#pragma unroll                // keeping the S fragments resident in registers)
   for (int ks = 0; ks < 4; ++ks) offB[ks] = member_off(4 * ks + c4);
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) offD[mt] = member_off(8 * mt + r4);
@@ -196,38 +231,56 @@ __global__ void __launch_bounds__(256, 2)
     for (int j = 0; j < 4; ++j) b = ((b & ~p.lo_mask[j]) << 1) | (b & p.lo_mask[j]);
     return b;
   };
-  auto load_tile = [&](uint64_t tl, double2* x) {
+  // highest in-tile position: the 3 tuple bits of a tile sit at the lowest free positions
+  int hi_tile = (int)p.pos[3];
+  for (int f = 0, nf = 0; f < 64 && nf < 3; ++f)
+    if (f != (int)p.pos[0] && f != (int)p.pos[1] && f != (int)p.pos[2] && f != (int)p.pos[3]) {
+      hi_tile = max(hi_tile, f);
+      ++nf;
+    }
+  // packed mode: the transpose of (tuple t, member m) is (pair_swap(t), pswap_c(m)); tiles
+  // whose elements are all stored in place (packed_tile_direct) skip the per-element test
+  auto tile_packed = [&](uint64_t tl) {
+    return p.mirror && !packed_tile_direct(base_of(tl * 8), hi_tile);
+  };
+  auto load_tile = [&](uint64_t tl, double2* x, bool packed) {
     const uint64_t t = tl * 8 + r4;
     if (tl < n_tiles && t < p.n_tuples) {
-      const double2* src = a + base_of(t);
+      const uint64_t b = base_of(t);
+      if (packed) {
+        const uint64_t bm = base_of(pair_swap(t));
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) x[ks] = src[offB[ks]];
+        for (int ks = 0; ks < 4; ++ks) {  // one load per element: select the address first
+          const uint64_t e = b + offB[ks], em = bm + member_off(pswap_c(4 * ks + c4));
+          const bool in_place = packed_stored(e, em);
+          const double2 v = a[in_place ? e : em];
+          x[ks] = in_place ? v : cj(v);
+        }
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) x[ks] = a[b + offB[ks]];
+      }
     } else {
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) x[ks] = make_double2(0.0, 0.0);
     }
   };
-
-  // mirror mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
-  auto valid = [&](uint64_t tl) {
-    if (!p.mirror) return true;
-    const uint64_t b = tl >> 1;
-    return b <= pair_swap(b);
-  };
+  // packed mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block);
+  // the two tiles of a block belong to warps 2j, 2j+1 of one CTA
   auto next_tile = [&](uint64_t tl) {
-    while (tl < n_tiles && !valid(tl)) tl += nwarps;
+    if (p.mirror)
+      while (tl < n_tiles && (tl >> 1) > pair_swap(tl >> 1)) tl += nwarps;
     return tl;
   };
-  uint64_t offDm[2];
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) offDm[mt] = member_off(pswap_c(8 * mt + r4));
 
   double2 xb_cur[4], xb_nxt[4];
   uint64_t tile = next_tile(warp);
-  load_tile(tile, xb_cur);
+  bool pk_cur = tile < n_tiles && tile_packed(tile);
+  load_tile(tile, xb_cur, pk_cur);
   while (tile < n_tiles) {
     const uint64_t nxt = next_tile(tile + nwarps);
-    load_tile(nxt, xb_nxt);  // register prefetch of the next tile
+    const bool pk_nxt = nxt < n_tiles && tile_packed(nxt);
+    load_tile(nxt, xb_nxt, pk_nxt);  // register prefetch of the next tile
     double p1[2][2], p2[2][2], p3[2][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -244,28 +297,41 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
     const uint64_t t0 = tile * 8 + 2 * c4;
-    const bool mir = p.mirror && (tile >> 1) != pair_swap(tile >> 1);
+    const bool self = p.mirror && (tile >> 1) == pair_swap(tile >> 1);
+    if (self) named_bar(1 + ((threadIdx.x >> 5) >> 1), 64);  // both tiles' loads are done
+    const uint64_t b0 = base_of(t0), b1 = base_of(t0 + 1);
+    uint64_t bm0 = 0, bm1 = 0;
+    if (pk_cur) {
+      bm0 = base_of(pair_swap(t0));
+      bm1 = base_of(pair_swap(t0 + 1));
+    }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const double2 y0 = make_double2(p1[mt][0] - p2[mt][0], p3[mt][0] - p1[mt][0] - p2[mt][0]);
       const double2 y1 = make_double2(p1[mt][1] - p2[mt][1], p3[mt][1] - p1[mt][1] - p2[mt][1]);
-      if constexpr (ADJ) {
-        if (t0 + 1 < p.n_tuples) {
-          st32(a + base_of(t0) + offD[mt], y0, y1);
-        } else if (t0 < p.n_tuples) {
-          a[base_of(t0) + offD[mt]] = y0;
+      const uint64_t e0 = b0 + offD[mt], e1 = b1 + offD[mt];
+      if (!pk_cur) {
+        if (ADJ && t0 + 1 < p.n_tuples) {
+          st32(a + e0, y0, y1);
+        } else {
+          if (t0 < p.n_tuples) a[e0] = y0;
+          if (t0 + 1 < p.n_tuples) a[e1] = y1;
         }
-      } else {
-        if (t0 < p.n_tuples) a[base_of(t0) + offD[mt]] = y0;
-        if (t0 + 1 < p.n_tuples) a[base_of(t0 + 1) + offD[mt]] = y1;
-      }
-      if (mir) {  // whole blocks only: n_tuples is a multiple of 16 in mirror mode
-        a[base_of(pair_swap(t0)) + offDm[mt]] = cj(y0);
-        a[base_of(pair_swap(t0 + 1)) + offDm[mt]] = cj(y1);
+      } else {  // slow path: per-element placement
+        const uint64_t om = member_off(pswap_c(8 * mt + r4));
+        if (t0 < p.n_tuples) {
+          if (packed_stored(e0, bm0 + om)) a[e0] = y0;
+          else if (!self) a[bm0 + om] = cj(y0);
+        }
+        if (t0 + 1 < p.n_tuples) {
+          if (packed_stored(e1, bm1 + om)) a[e1] = y1;
+          else if (!self) a[bm1 + om] = cj(y1);
+        }
       }
     }
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) xb_cur[ks] = xb_nxt[ks];
+    pk_cur = pk_nxt;
     tile = nxt;
   }
 }
@@ -477,29 +543,36 @@ __device__ __forceinline__ void group_sub_k1(double2* X, const double2* F, const
   }
 }
 
+// Packed-mode copy helpers shared by the group and tile kernels.  An element at tile-relative
+// offset off has its transpose at pair_swap(off) relative to pair_swap(base) (pair_swap is a
+// bit permutation, so it distributes over the disjoint base / offset bits).
+
 // NQ group qubits, WARPS warps per CTA (one CTA per SM), NBUF tile buffers per warp
 // (2 = cp.async double buffering), HAS3: the program may contain a dense k=3 sub-op (needs
-// the register budget of 8 warps), UI: n-tiles per k=2 pass, PMAX: program capacity.
-template <int NQ, int WARPS, int NBUF, bool HAS3, int UI, int PMAX>
+// the register budget of 8 warps), UI: n-tiles per k=2 pass.
+// Packed mode (p.mirror): only tiles of canonical 16-tuple blocks are processed; every element
+// is read from, and written to, the one of {itself, its transpose} the packed layout keeps.
+// A self-transposed block spans 16 / T warp tiles that read each other's elements: those warps
+// meet at a named barrier between their loads and their stores.
+template <int NQ, int WARPS, int NBUF, bool HAS3, int UI>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     group_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
   constexpr int MB = 2 * NQ, TB = 9 - MB, T = 1 << TB;
+  constexpr int WPB = 16 / T;  // warp tiles per 16-tuple block
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // shared: program (<= PMAX double2) | X tiles WARPS x NBUF x 512 double2 |
+  // shared: program | X tiles WARPS x NBUF x 512 double2 |
   //         copy tables | sub-op headers
   double2* sProg = reinterpret_cast<double2*>(smem_raw);
-  double2* sX = sProg + PMAX;
-  // copy mapping tables: iteration i (16) -> (tuple bits, member bits, address offset)
+  double2* sX = sProg + ((p.prog_elems + 7) & ~7);
+  // copy tables: iteration i (16) -> offset [i], transpose offset [16 + i], tuple/member bits
   uint64_t* sIterOff = reinterpret_cast<uint64_t*>(sX + WARPS * NBUF * 512);  // [2][16]
-  int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);                          // [2][16]
+  int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);                          // [16]
   GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // The 9 index bits of a tile element (TB tuple bits at the lowest free physical positions,
   // MB member bits at pos[]) sorted by physical position: lanes take the 5 lowest, the copy
   // iterations the next 4, so every copy instruction covers the most contiguous addresses.
-  // Mirror mode writes each element (t, m) conjugated to its transpose position: tuple bit j
-  // lands on free position f[j^1], member bit j on pos[j^1].
   int freep[4];
   {
     int nf = 0;
@@ -509,14 +582,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if (!tgt) freep[nf++] = f;
     }
   }
-  auto build_map = [&](bool mir, int& ltm, uint64_t& loff, int* it_tm, uint64_t* it_off) {
+  int lane_tm;
+  uint64_t lane_off;
+  {
     int bit_pos[9], bit_id[9];  // id < TB: tuple bit, else member bit id-TB
     for (int j = 0; j < TB; ++j) {
-      bit_pos[j] = freep[mir ? (j ^ 1) : j];
+      bit_pos[j] = freep[j];
       bit_id[j] = j;
     }
     for (int j = 0; j < MB; ++j) {
-      bit_pos[TB + j] = (int)p.pos[mir ? (j ^ 1) : j];
+      bit_pos[TB + j] = (int)p.pos[j];
       bit_id[TB + j] = TB + j;
     }
     for (int x = 1; x < 9; ++x)  // insertion sort by position
@@ -535,22 +610,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         }
       return t | (m << TB);
     };
-    ltm = tm_of(lane, 0, 5, loff);
-    if (threadIdx.x < 16) it_tm[threadIdx.x] = tm_of(threadIdx.x, 5, 4, it_off[threadIdx.x]);
-  };
-  // address of (tile, t, m) = base(tile*T) + deposit(t at free bits) + deposit(m at pos[]):
-  // insert_zeros is a bit deposit, so the tuple and member parts add independently.
-  int lane_tm, mlane_tm = 0;
-  uint64_t lane_off, mlane_off = 0;
-  build_map(false, lane_tm, lane_off, sIterTM, sIterOff);
-  if (p.mirror) build_map(true, mlane_tm, mlane_off, sIterTM + 16, sIterOff + 16);
+    lane_tm = tm_of(lane, 0, 5, lane_off);
+    if (threadIdx.x < 16) {
+      sIterTM[threadIdx.x] = tm_of(threadIdx.x, 5, 4, sIterOff[threadIdx.x]);
+      sIterOff[16 + threadIdx.x] = pair_swap(sIterOff[threadIdx.x]);
+    }
+  }
+  const uint64_t lane_poff = pair_swap(lane_off);
+  const int hi_tile = max(freep[TB - 1], (int)p.pos[MB - 1]);  // highest in-tile position
   for (int e = threadIdx.x; e < p.prog_elems; e += blockDim.x) sProg[e] = p.prog[e];
   for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
   __syncthreads();
 
   const uint64_t n_tiles = (p.n_tuples + T - 1) >> TB;
   const uint64_t tile_stride = (uint64_t)gridDim.x * WARPS;
-  // mirror mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
+  // packed mode: only tiles of canonical 16-tuple blocks (block b <= its transpose block)
   auto block_of = [&](uint64_t tl) { return (tl << TB) >> 4; };
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
@@ -560,44 +634,60 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   uint64_t tile = next_tile((uint64_t)blockIdx.x * WARPS + warp);
   double2* const wbuf = sX + warp * NBUF * 512;  // NBUF 512-double2 tiles (no indexed array:
                                                   // a dynamically indexed pointer array spills)
-  // element (lane, i): tuple t, member m, address base(tile*T) + off
-  auto elem = [&](int i, int& t, int& m, uint64_t& off) {
-    const int tm = lane_tm | sIterTM[i];
-    t = tm & (T - 1);
-    m = tm >> TB;
-    off = lane_off + sIterOff[i];
-  };
+  // issue the tile's copies; returns the mask of elements copied from transpose positions
   auto issue_load = [&](uint64_t tl, double2* buf) {
-    const double2* src = a + insert_zeros(tl << TB, p.lo_mask, MB);
+    const uint64_t tb0 = insert_zeros(tl << TB, p.lo_mask, MB);
+    const uint64_t base = tb0 + lane_off, pbase = pair_swap(tb0) + lane_poff;
+    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+    unsigned mask = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      int t, m;
-      uint64_t off;
-      elem(i, t, m, off);
+      const int tm = lane_tm | sIterTM[i];
+      const int t = tm & (T - 1), m = tm >> TB;
       const bool ok = (tl << TB) + t < p.n_tuples;
-      cp_async16(buf + xs_idx<T>(m, t), ok ? src + off : a, ok);
+      uint64_t src = base + sIterOff[i];
+      if (packed) {
+        const uint64_t srcm = pbase + sIterOff[16 + i];
+        if (!packed_stored(src, srcm)) {
+          src = srcm;
+          mask |= 1u << i;
+        }
+      }
+      cp_async16(buf + xs_idx<T>(m, t), ok ? a + src : a, ok);
     }
     cp_async_commit();
+    return mask;
+  };
+  auto fixup = [&](double2* buf, unsigned mask) {
+    for (; mask; mask &= mask - 1) {
+      const int tm = lane_tm | sIterTM[__ffs(mask) - 1];
+      double* im = &buf[xs_idx<T>(tm >> TB, tm & (T - 1))].y;
+      *im = -*im;
+    }
   };
 
-  if (NBUF == 2 && tile < n_tiles) issue_load(tile, wbuf);
+  unsigned mask_next = 0;
+  if (NBUF == 2 && tile < n_tiles) mask_next = issue_load(tile, wbuf);
   int cur = 0;
   for (; tile < n_tiles; tile = next_tile(tile + tile_stride)) {
+    unsigned mask;
     if constexpr (NBUF == 2) {
+      mask = mask_next;
       const uint64_t next = next_tile(tile + tile_stride);
       if (next < n_tiles) {
-        issue_load(next, wbuf + ((cur ^ 1) << 9));
+        mask_next = issue_load(next, wbuf + ((cur ^ 1) << 9));
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
     } else {
-      issue_load(tile, wbuf);
+      mask = (p.dbg & 2) ? 0u : issue_load(tile, wbuf);
       cp_async_wait<0>();
     }
-    __syncwarp();
     double2* X = wbuf + (NBUF == 2 ? (cur << 9) : 0);
-    for (int s = 0; s < p.n_sub; ++s) {
+    fixup(X, mask);
+    __syncwarp();
+    for (int s = 0; s < (p.dbg & 1 ? 0 : p.n_sub); ++s) {
       const GroupSub& g = sSub[s];
       const double2* F = sProg + g.s_off;
       if (g.k == 2) {
@@ -609,21 +699,25 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
       __syncwarp();
     }
-    {
-      double2* dst = a + insert_zeros(tile << TB, p.lo_mask, MB);
+    const bool self = p.mirror && block_of(tile) == pair_swap(block_of(tile));
+    if (self) named_bar(1 + warp / WPB, 32 * WPB);  // the block's loads are all done
+    if (!(p.dbg & 2)) {
+      const uint64_t tb0 = insert_zeros(tile << TB, p.lo_mask, MB);
+      const uint64_t base = tb0 + lane_off, pbase = pair_swap(tb0) + lane_poff;
+      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        int t, m;
-        uint64_t off;
-        elem(i, t, m, off);
-        if ((tile << TB) + t < p.n_tuples) dst[off] = X[xs_idx<T>(m, t)];
-      }
-      if (p.mirror && block_of(tile) != pair_swap(block_of(tile))) {  // conj to transposes
-        double2* dstm = a + insert_zeros(pair_swap(tile << TB), p.lo_mask, MB);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int tm = mlane_tm | sIterTM[16 + i];
-          dstm[mlane_off + sIterOff[16 + i]] = cj(X[xs_idx<T>(tm >> TB, tm & (T - 1))]);
+        const int tm = lane_tm | sIterTM[i];
+        const int t = tm & (T - 1), m = tm >> TB;
+        if ((tile << TB) + t >= p.n_tuples) continue;
+        const uint64_t dst = base + sIterOff[i];
+        const double2 v = X[xs_idx<T>(m, t)];
+        if (!packed) {
+          a[dst] = v;
+        } else {
+          const uint64_t dstm = pbase + sIterOff[16 + i];
+          if (packed_stored(dst, dstm)) a[dst] = v;
+          else if (!self) a[dstm] = cj(v);  // self block: the transpose is stored directly
         }
       }
     }
@@ -632,16 +726,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
 }
 
-template <int NQ, int WARPS, int NBUF, bool HAS3, int UI, int PMAX = kGroupProgMax>
+template <int NQ, int WARPS, int NBUF, bool HAS3, int UI>
+static size_t group_smem(const GroupParams& p) {
+  return (size_t)((p.prog_elems + 7) & ~7) * sizeof(double2) +
+         (size_t)WARPS * NBUF * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
+         (size_t)p.n_sub * sizeof(GroupSub);
+}
+
+template <int NQ, int WARPS, int NBUF, bool HAS3, int UI>
 static cudaError_t launch_group_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
   static bool attr_set = false;
   constexpr int T = 1 << (9 - 2 * NQ);
-  const size_t smem = (size_t)PMAX * sizeof(double2) +
-                      (size_t)WARPS * NBUF * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
-                      (size_t)kMaxSub * sizeof(GroupSub);
-  auto kern = group_kernel<NQ, WARPS, NBUF, HAS3, UI, PMAX>;
+  const size_t smem = group_smem<NQ, WARPS, NBUF, HAS3, UI>(p);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = group_kernel<NQ, WARPS, NBUF, HAS3, UI>;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -665,18 +765,19 @@ static cudaError_t launch_group_cfg(double2* a, const GroupParams& p, cudaStream
 // any member positions, against 4.1-4.9 TB/s for 8-tuple warp tiles whose members sit at
 // position >= 6).  Warp w computes on tuples [wT, (w+1)T) of the tile with the sub-op code
 // above; only the copies are shared.
-// Mirror mode: canonical unit = block of 2^BB tiles (BB = TTB & 1, so the block index starts
-// at an even tuple bit); a block is processed when block <= pair_swap(block), and writes
-// conjugates to the transposed block unless it is its own transpose.
+// Packed mode needs TTB even (8 warps: 256 / 64 / 16 tuples): a tile is then a whole
+// transpose block -- processed when tile <= pair_swap(tile), self-transposed tiles entirely
+// inside one CTA, so its loads finish (barrier) before any of its stores.
 // ------------------------------------------------------------------------------------
 template <int NQ, int WARPS, int NBUF, int UI>
 __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
     tile_kernel(double2* __restrict__ a, const __grid_constant__ GroupParams p) {
   constexpr int MB = 2 * NQ, TB = 9 - MB, T = 1 << TB;
-  constexpr int WB = WARPS == 8 ? 3 : (WARPS == 4 ? 2 : 1), TTB = TB + WB, TT = 1 << TTB;
-  constexpr int HB = 5 + WB, NBITS = HB + 4, BB = TTB & 1, ELEMS = WARPS * 512;
+  constexpr int WB = WARPS == 16 ? 4 : (WARPS == 8 ? 3 : (WARPS == 4 ? 2 : 1));
+  constexpr int TTB = TB + WB, TT = 1 << TTB;
+  constexpr int HB = 5 + WB, NBITS = HB + 4, ELEMS = WARPS * 512;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // shared: program | NBUF tiles | copy tables [2][16] | sub-op headers
+  // shared: program | NBUF tiles | copy tables (offset [16], transpose offset [16], bits) | subs
   const int prog_cap = (p.prog_elems + 7) & ~7;
   double2* sProg = reinterpret_cast<double2*>(smem_raw);
   double2* sX = sProg + prog_cap;
@@ -684,26 +785,31 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
   int* sIterTM = reinterpret_cast<int*>(sIterOff + 32);
   GroupSub* sSub = reinterpret_cast<GroupSub*>(sIterTM + 32);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (TTB & 1) {
+    if (p.mirror) __trap();  // the host never launches packed mode with odd TTB
+  }
 
-  int freep[TTB + 1];
+  int freep[TTB];
   {
     int nf = 0;
-    for (int f = 0; f < 64 && nf < TTB + 1; ++f) {
+    for (int f = 0; f < 64 && nf < TTB; ++f) {
       bool tgt = false;
       for (int j = 0; j < MB; ++j) tgt |= (int)p.pos[j] == f;
       if (!tgt) freep[nf++] = f;
     }
   }
   // NBITS tile bits sorted by physical position: threads take the HB lowest, iterations the
-  // next 4.  Mirror map: tuple bit j lands on freep[j^1], member bit j on pos[j^1].
-  auto build_map = [&](bool mir, int& ttm, uint64_t& toff, int* it_tm, uint64_t* it_off) {
+  // next 4.
+  int thr_tm;
+  uint64_t thr_off;
+  {
     int bit_pos[NBITS], bit_id[NBITS];  // id < TTB: tuple bit, else member bit id-TTB
     for (int j = 0; j < TTB; ++j) {
-      bit_pos[j] = freep[mir ? (j ^ 1) : j];
+      bit_pos[j] = freep[j];
       bit_id[j] = j;
     }
     for (int j = 0; j < MB; ++j) {
-      bit_pos[TTB + j] = (int)p.pos[mir ? (j ^ 1) : j];
+      bit_pos[TTB + j] = (int)p.pos[j];
       bit_id[TTB + j] = TTB + j;
     }
     for (int x = 1; x < NBITS; ++x)
@@ -722,13 +828,14 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
         }
       return t | (m << TTB);
     };
-    ttm = tm_of(threadIdx.x, 0, HB, toff);
-    if (threadIdx.x < 16) it_tm[threadIdx.x] = tm_of(threadIdx.x, HB, 4, it_off[threadIdx.x]);
-  };
-  int thr_tm, mthr_tm = 0;
-  uint64_t thr_off, mthr_off = 0;
-  build_map(false, thr_tm, thr_off, sIterTM, sIterOff);
-  if (p.mirror) build_map(true, mthr_tm, mthr_off, sIterTM + 16, sIterOff + 16);
+    thr_tm = tm_of(threadIdx.x, 0, HB, thr_off);
+    if (threadIdx.x < 16) {
+      sIterTM[threadIdx.x] = tm_of(threadIdx.x, HB, 4, sIterOff[threadIdx.x]);
+      sIterOff[16 + threadIdx.x] = pair_swap(sIterOff[threadIdx.x]);
+    }
+  }
+  const uint64_t thr_poff = pair_swap(thr_off);
+  const int hi_tile = max(freep[TTB - 1], (int)p.pos[MB - 1]);  // highest in-tile position
   for (int e = threadIdx.x; e < p.prog_elems; e += blockDim.x) sProg[e] = p.prog[e];
   for (int e = threadIdx.x; e < p.n_sub; e += blockDim.x) sSub[e] = p.sub[e];
   __syncthreads();
@@ -736,7 +843,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
   const uint64_t n_tiles = (p.n_tuples + TT - 1) >> TTB;
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
-      while (tl < n_tiles && (tl >> BB) > pair_swap(tl >> BB)) tl += gridDim.x;
+      while (tl < n_tiles && tl > pair_swap(tl)) tl += gridDim.x;
     return tl;
   };
   // shared index of tile element (tuple t, member m): warp sub-tile t / T, swizzled inside
@@ -745,31 +852,52 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
     return ((t >> TB) << 9) + xs_idx<T>(m, t & (T - 1));
   };
   auto issue_load = [&](uint64_t tl, double2* buf) {
-    const double2* src = a + insert_zeros(tl << TTB, p.lo_mask, MB) + thr_off;
+    const uint64_t tb0 = insert_zeros(tl << TTB, p.lo_mask, MB);
+    const uint64_t base = tb0 + thr_off, pbase = pair_swap(tb0) + thr_poff;
+    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+    unsigned mask = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int tm = thr_tm | sIterTM[i];
       const bool ok = (tl << TTB) + (tm & (TT - 1)) < p.n_tuples;
-      cp_async16(buf + sidx(tm), ok ? src + sIterOff[i] : a, ok);
+      uint64_t src = base + sIterOff[i];
+      if (packed) {
+        const uint64_t srcm = pbase + sIterOff[16 + i];
+        if (!packed_stored(src, srcm)) {
+          src = srcm;
+          mask |= 1u << i;
+        }
+      }
+      cp_async16(buf + sidx(tm), ok ? a + src : a, ok);
     }
     cp_async_commit();
+    return mask;
+  };
+  auto fixup = [&](double2* buf, unsigned mask) {  // conj of the transposed copies
+    for (; mask; mask &= mask - 1) {
+      double* im = &buf[sidx(thr_tm | sIterTM[__ffs(mask) - 1])].y;
+      *im = -*im;
+    }
   };
 
   // NBUF = 2: the next tile's copies are issued right after the barrier that makes the current
   // tile visible, so they overlap the compute and the stores (2 barriers per tile).
   uint64_t tile = next_tile(blockIdx.x);
-  if (NBUF == 2 && tile < n_tiles) issue_load(tile, sX);
+  unsigned mask_next = 0;
+  if (NBUF == 2 && tile < n_tiles) mask_next = issue_load(tile, sX);
   int cur = 0;
   while (tile < n_tiles) {
     const uint64_t next = next_tile(tile + gridDim.x);
-    if constexpr (NBUF == 1) issue_load(tile, sX);
+    double2* buf = sX + (NBUF == 2 ? cur * ELEMS : 0);
+    unsigned mask = mask_next;
+    if constexpr (NBUF == 1) mask = (p.dbg & 2) ? 0u : issue_load(tile, sX);
     cp_async_wait<0>();
+    fixup(buf, mask);
     __syncthreads();  // current tile visible; the other buffer's stores are done
     if constexpr (NBUF == 2)
-      if (next < n_tiles) issue_load(next, sX + (cur ^ 1) * ELEMS);
-    double2* buf = sX + (NBUF == 2 ? cur * ELEMS : 0);
+      if (next < n_tiles) mask_next = issue_load(next, sX + (cur ^ 1) * ELEMS);
     double2* X = buf + (warp << 9);
-    for (int s = 0; s < p.n_sub; ++s) {
+    for (int s = 0; s < (p.dbg & 1 ? 0 : p.n_sub); ++s) {
       const GroupSub& g = sSub[s];
       const double2* F = sProg + g.s_off;
       if (g.k == 2)
@@ -779,19 +907,24 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
       __syncwarp();
     }
     __syncthreads();
-    {
-      double2* dst = a + insert_zeros(tile << TTB, p.lo_mask, MB) + thr_off;
+    if (!(p.dbg & 2)) {
+      const uint64_t tb0 = insert_zeros(tile << TTB, p.lo_mask, MB);
+      const uint64_t base = tb0 + thr_off, pbase = pair_swap(tb0) + thr_poff;
+      const bool self = pair_swap(tile) == tile;
+      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int tm = thr_tm | sIterTM[i];
-        if ((tile << TTB) + (tm & (TT - 1)) < p.n_tuples) dst[sIterOff[i]] = buf[sidx(tm)];
-      }
-      const uint64_t blk = tile >> BB;
-      if (p.mirror && pair_swap(blk) != blk) {  // conjugates to the transposed block
-        double2* dstm = a + insert_zeros(pair_swap(tile << TTB), p.lo_mask, MB) + mthr_off;
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          dstm[sIterOff[16 + i]] = cj(buf[sidx(mthr_tm | sIterTM[16 + i])]);
+        if ((tile << TTB) + (tm & (TT - 1)) >= p.n_tuples) continue;
+        const uint64_t dst = base + sIterOff[i];
+        const double2 v = buf[sidx(tm)];
+        if (!packed) {
+          a[dst] = v;
+        } else {
+          const uint64_t dstm = pbase + sIterOff[16 + i];
+          if (packed_stored(dst, dstm)) a[dst] = v;
+          else if (!self) a[dstm] = cj(v);  // self tile: the transpose is stored directly
+        }
       }
     }
     if constexpr (NBUF == 1) __syncthreads();  // the buffer is reloaded next
@@ -799,8 +932,6 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
     cur ^= 1;
   }
 }
-
-static int g_tile_mode = -1;  // env TANQ_GROUP=warp: the per-warp group_kernel (comparison)
 
 template <int NQ, int WARPS, int NBUF, int UI>
 static cudaError_t launch_tile_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
@@ -828,55 +959,76 @@ static cudaError_t launch_tile_cfg(double2* a, const GroupParams& p, cudaStream_
   return cudaGetLastError();
 }
 
+static int g_tile_mode = -1;  // env TANQ_GROUP = auto | warp | q1 | o1 (experiments)
+
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
-  if (g_tile_mode < 0) {  // env TANQ_GROUP = auto | warp | q1 | q2 | p1 | p2 (experiments)
+  if (g_tile_mode < 0) {
     const char* e = getenv("TANQ_GROUP");
-    g_tile_mode = !e ? -2
-                     : !strcmp(e, "warp") ? 0
-                     : !strcmp(e, "q1")   ? 1
-                     : !strcmp(e, "q2")   ? 2
-                     : !strcmp(e, "p1")   ? 3
-                     : !strcmp(e, "p2")   ? 4 : -2;
+    g_tile_mode = !e ? 9 : !strcmp(e, "warp") ? 0 : !strcmp(e, "q1") ? 1 : !strcmp(e, "o1") ? 2
+                : !strcmp(e, "w12") ? 3 : !strcmp(e, "w8") ? 4 : 9;
   }
   bool has3 = false;
-  for (int i = 0; i < p.n_sub; ++i) has3 |= p.sub[i].k == 3;
+  int n2 = 0;
+  uint32_t lo = 64;
+  for (int i = 0; i < p.n_sub; ++i) {
+    has3 |= p.sub[i].k == 3;
+    n2 += p.sub[i].k == 2;
+  }
+  for (int j = 0; j < 2 * p.nq; ++j) lo = p.pos[j] < lo ? p.pos[j] : lo;
   // dense 64x64 sub-ops are DMMA-bound: per-warp tiles, 2 buffers, 8 independent warps
   if (has3 && p.nq != 3) return cudaErrorInvalidValue;  // the planner never emits this
   if (has3) return launch_group_cfg<3, 8, 2, true, 4>(a, p, st);
   int mode = g_tile_mode;
-  if (mode == -2) {
-    // auto (measured at n = 16, scripts/kbench.py): cooperative tiles win while the group is
-    // memory-bound (<= 2 k=2 sub-ops) and its lowest member position is >= 6 (per-warp tiles
-    // then read 128 B runs, microbench/locality.cu); heavier programs are DMMA-bound and run
-    // best on 16 independent warps.
-    uint32_t lo = 64;
-    for (int j = 0; j < 2 * p.nq; ++j) lo = p.pos[j] < lo ? p.pos[j] : lo;
-    int n2 = 0;
-    for (int i = 0; i < p.n_sub; ++i) n2 += p.sub[i].k == 2;
-    mode = (p.nq == 2 || (lo > 5 && n2 <= 2)) ? 1 : 0;
+  if (mode == 9) {
+    // auto (measured at n = 16, scripts/kbench.py).  Full layout: cooperative tiles while the
+    // group is memory-bound (<= 2 k=2 sub-ops) and its lowest member position is >= 6
+    // (per-warp tiles then read 128 B runs, microbench/locality.cu); heavier programs are
+    // DMMA-bound and run best on 16 independent warps.  Packed layout (half the traffic):
+    // 3-qubit groups are DMMA-bound -> 16 independent warps; 4-qubit groups need the 8-warp
+    // tile for contiguous copies (per-warp tiles hold 2 tuples).
+    if (p.mirror)
+      mode = p.nq == 3 ? 0 : 2;
+    else
+      mode = (p.nq == 2 || (lo > 5 && n2 <= 2)) ? 1 : 0;
   }
   if (p.nq == 2 && mode == 0) mode = 1;
+  if (p.mirror && mode == 1) mode = 2;  // packed mode needs whole transpose blocks per tile
+  if (p.nq == 2 && (mode == 3 || mode == 4)) mode = p.mirror ? 2 : 1;
+  if (mode == 3 && group_smem<3, 12, 2, false, 2>(p) > 227 * 1024) mode = 0;
   switch (mode) {
     case 0:
       if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);
       return launch_group_cfg<3, 16, 1, false, 2>(a, p, st);
-    case 2:
-      if (p.nq == 2) return launch_tile_cfg<2, 4, 2, 2>(a, p, st);
-      if (p.nq == 4) return launch_tile_cfg<4, 4, 2, 1>(a, p, st);
-      return launch_tile_cfg<3, 4, 2, 2>(a, p, st);
-    case 3:
-      if (p.nq == 2) return launch_tile_cfg<2, 2, 1, 2>(a, p, st);
-      if (p.nq == 4) return launch_tile_cfg<4, 2, 1, 1>(a, p, st);
-      return launch_tile_cfg<3, 2, 1, 2>(a, p, st);
+    case 3:  // (4-qubit transpose blocks span 8 warp tiles: 8 warps per CTA)
+      if (p.nq == 4) return launch_group_cfg<4, 8, 2, false, 1>(a, p, st);
+      return launch_group_cfg<3, 12, 2, false, 2>(a, p, st);
     case 4:
-      if (p.nq == 2) return launch_tile_cfg<2, 2, 2, 2>(a, p, st);
-      if (p.nq == 4) return launch_tile_cfg<4, 2, 2, 1>(a, p, st);
-      return launch_tile_cfg<3, 2, 2, 2>(a, p, st);
+      if (p.nq == 4) return launch_group_cfg<4, 8, 2, false, 1>(a, p, st);
+      return launch_group_cfg<3, 8, 2, false, 2>(a, p, st);
+    case 2:
+      if (p.nq == 2) return launch_tile_cfg<2, 8, 1, 2>(a, p, st);
+      if (p.nq == 4) return launch_tile_cfg<4, 8, 1, 1>(a, p, st);
+      return launch_tile_cfg<3, 8, 1, 2>(a, p, st);
     default:
       if (p.nq == 2) return launch_tile_cfg<2, 4, 1, 2>(a, p, st);
       if (p.nq == 4) return launch_tile_cfg<4, 4, 1, 1>(a, p, st);
       return launch_tile_cfg<3, 4, 1, 2>(a, p, st);
   }
+}
+
+// Packed -> full layout: every element the packed layout does not keep gets conj(transpose).
+__global__ void unpack_kernel(double2* __restrict__ a, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
+    const uint64_t em = pair_swap(e);
+    if (!packed_stored(e, em)) a[e] = cj(a[em]);
+  }
+}
+
+cudaError_t launch_unpack(double2* a, int L, cudaStream_t st) {
+  const uint64_t n = (uint64_t)1 << L;
+  unpack_kernel<<<grid_for(n, kThreads, 148ull * 16), kThreads, 0, st>>>(a, n);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------

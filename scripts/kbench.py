@@ -8,12 +8,16 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("KBENCH_PKG_ROOT"):  # A/B runs against another build of the package
+    sys.path.insert(0, os.environ["KBENCH_PKG_ROOT"])
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=14)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--kmax", type=int, default=3, help="group size limit for the group cases")
+    ap.add_argument("--groups-only", action="store_true")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -29,7 +33,7 @@ def main():
         torch.cuda.set_stream(st)
         sim.set_stream(st.cuda_stream)
         import workloads as W
-        for qs in cases:
+        for qs in ([] if args.groups_only else cases):
             k = len(qs)
             Ks = W.random_kraus(rng, 2 ** k, 2)  # CPTP: Hermiticity-preserving (mirror mode)
             for _ in range(3):
@@ -50,9 +54,12 @@ def main():
         groups = [[(0, 1), (1, 2)], [(1, 2), (2, 3), (1, 3)], [(5, n - 1), (n - 1, n - 2)],
                   [(0, 1), (1, 2), (0, 2), (2, 1)], [(3, 7), (7, n - 1), (3, n - 1), (7, 3), (3, 7)],
                   [(8, 10), (10, 12), (8, 12)], [(n - 3, n - 2), (n - 2, n - 1), (n - 3, n - 1), (n - 2, n - 3)]]
+        if args.kmax >= 4:  # 4-qubit groups
+            groups += [[(0, 1), (2, 3), (1, 2), (0, 3)], [(n - 4, n - 3), (n - 2, n - 1), (n - 3, n - 2), (n - 4, n - 1)],
+                       [(5, 9), (11, 13), (9, 11), (5, 13)]]
         for g in groups:
             ops = [W.Op("kraus", qs, kraus=W.random_kraus(rng, 4, 2)) for qs in g]
-            plan = sim.plan(W.Circuit(n, ops), None, fuse=2, k_max=3)
+            plan = sim.plan(W.Circuit(n, ops), None, fuse=2, k_max=args.kmax)
             info = plan.info()
             for _ in range(3):
                 plan.exec(sim)

@@ -33,7 +33,11 @@ for seed in range(4):
         for mirror in (True, False):
             with Simulator(n) as sim:
                 sim.run_circuit(c, nm, fuse=2, k_max=kmax, mirror=mirror)
+                p = sim.probs()                   # diagonal: valid in the packed layout
+                z = sim.expect_pauli(0, 0b11)
                 got = sim.get_state().reshape(N, N).T
+            np.testing.assert_allclose(p, np.diag(ref).real, atol=1e-10)
+            assert abs(z - dense.expect_pauli(ref, n, 0, 0b11)) < 1e-10
             d = got - ref
             mx = np.abs(d).max()
             rel = np.linalg.norm(d) / np.linalg.norm(ref)
@@ -43,13 +47,15 @@ print("OK", worst)
 """
 
 
-@pytest.mark.parametrize("group,k2path", [("warp", "direct"), ("q1", "tile"), ("q2", "tile"),
-                                          ("p1", "tile"), ("p2", "auto"), ("auto", "auto")])
-def test_kernel_variant_parity(group, k2path):
+@pytest.mark.parametrize("group,k2path,mirror", [
+    ("warp", "direct", "1"), ("q1", "tile", "1"), ("o1", "auto", "1"), ("auto", "auto", "1"),
+    ("auto", "direct", "0"), ("q1", "auto", "0"), ("warp", "tile", "0"), ("w12", "auto", "1"),
+    ("w8", "auto", "1"), ("w12", "auto", "0")])
+def test_kernel_variant_parity(group, k2path, mirror):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path)
+    env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path, TANQ_MIRROR=mirror)
     r = subprocess.run([sys.executable, "-c", SNIPPET % {"root": ROOT}], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]

@@ -289,8 +289,8 @@ def run_ours(args):
               "fp64_peak_kind": peak_tf_kind,
               "floors_ms": {"hbm": t_hbm * 1e3, "fp64": t_fp * 1e3},
               "flops_note": "algorithmic flops = 8 per complex multiply-add; the DMMA kernels "
-                            "execute 6 (3-multiply complex product); mirrored launches count "
-                            "24 B and half the flops per amplitude"}
+                            "execute 6 (3-multiply complex product); packed-layout launches "
+                            "count 16 B and half the flops per amplitude"}
     if t_fp > t_hbm:
         roofline = {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": tf / peak_tf, "peak_kind": peak_tf_kind, **common}

@@ -284,15 +284,16 @@ struct FusedOp {
   std::vector<FusedOp> sub;  // k=3 factored group: sub-ops applied in order in one pass
 };
 
-// B200 cost model in units of one K1 pass over the state (mirror mode: 24 B / amplitude),
-// DESIGN.md §6, calibrated with scripts/kbench.py at n = 16 on B200 (profiles/r01_kbench_n16*):
-// K1 16.4 ms = 1, K2 17.1-17.5 ms (~1.05; high targets on cooperative tiles), a dense k=3 op on
-// DMMA 34.8 ms (2.12, FP64 bound).  A factored group costs 0.45 + its sub-ops' FP64 time:
-// 0.38 per k=2 sub-op (2 ops 1.21-1.34, 3 ops 1.55-1.75, 4 ops 1.96-1.98), k=1 ~0.06.
-double sep_cost(int k) { return k == 1 ? 1.0 : (k == 2 ? 1.05 : 2.12); }
-double sub_cost(int k) { return k == 1 ? 0.06 : (k == 2 ? 0.38 : 2.12); }
-constexpr double kGroupBase = 0.45;
-double op_cost(int k) { return k <= 2 ? 1.0 : 2.12; }
+// B200 cost model in units of one K1 pass over the state, calibrated with
+// scripts/kbench.py at n = 16 on B200 in the packed Hermitian layout (16 B / amplitude per
+// pass; profiles/r01_kbench_n16_packed.jsonl): K1 10.6 ms = 1, K2 11.6-12.2 ms (low targets,
+// register stream) / 17.4-18.6 ms (a high target), ~1.4 on average; a dense k=3 op on DMMA
+// 37-40 ms (3.6, FP64 bound).  A factored group costs 0.55 + 0.62 per k=2 sub-op (2 ops
+// 1.70-1.92, 3 ops 2.29-2.43, 4 ops 2.95-3.05): DMMA-bound, the copies overlap.
+double sep_cost(int k) { return k == 1 ? 1.0 : (k == 2 ? 1.4 : 3.6); }
+double sub_cost(int k) { return k == 1 ? 0.1 : (k == 2 ? 0.62 : 3.6); }
+constexpr double kGroupBase = 0.55;
+double op_cost(int k) { return k <= 2 ? 1.0 : 3.6; }
 
 bool shares(const FusedOp& a, const int* q, int k) {
   for (int i = 0; i < a.k; ++i)

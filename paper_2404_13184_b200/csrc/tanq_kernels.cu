@@ -964,8 +964,7 @@ static int g_tile_mode = -1;  // env TANQ_GROUP = auto | warp | q1 | o1 (experim
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
   if (g_tile_mode < 0) {
     const char* e = getenv("TANQ_GROUP");
-    g_tile_mode = !e ? 9 : !strcmp(e, "warp") ? 0 : !strcmp(e, "q1") ? 1 : !strcmp(e, "o1") ? 2
-                : !strcmp(e, "w12") ? 3 : !strcmp(e, "w8") ? 4 : 9;
+    g_tile_mode = !e ? 9 : !strcmp(e, "warp") ? 0 : !strcmp(e, "q1") ? 1 : !strcmp(e, "o1") ? 2 : 9;
   }
   bool has3 = false;
   int n2 = 0;
@@ -993,18 +992,10 @@ cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
   }
   if (p.nq == 2 && mode == 0) mode = 1;
   if (p.mirror && mode == 1) mode = 2;  // packed mode needs whole transpose blocks per tile
-  if (p.nq == 2 && (mode == 3 || mode == 4)) mode = p.mirror ? 2 : 1;
-  if (mode == 3 && group_smem<3, 12, 2, false, 2>(p) > 227 * 1024) mode = 0;
   switch (mode) {
     case 0:
       if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);
       return launch_group_cfg<3, 16, 1, false, 2>(a, p, st);
-    case 3:  // (4-qubit transpose blocks span 8 warp tiles: 8 warps per CTA)
-      if (p.nq == 4) return launch_group_cfg<4, 8, 2, false, 1>(a, p, st);
-      return launch_group_cfg<3, 12, 2, false, 2>(a, p, st);
-    case 4:
-      if (p.nq == 4) return launch_group_cfg<4, 8, 2, false, 1>(a, p, st);
-      return launch_group_cfg<3, 8, 2, false, 2>(a, p, st);
     case 2:
       if (p.nq == 2) return launch_tile_cfg<2, 8, 1, 2>(a, p, st);
       if (p.nq == 4) return launch_tile_cfg<4, 8, 1, 1>(a, p, st);

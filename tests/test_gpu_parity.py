@@ -410,3 +410,45 @@ def test_dist_handle_world1(Sim):
         sim.run_circuit(c, nm)
         assert_parity(rho_of(sim, 6), dense.run(c, nm))
         assert sim.info()["world_size"] == 1
+
+
+def test_packed_layout_transitions(Sim):
+    """Packed Hermitian layout bookkeeping: diagonal reads stay packed, X/Y expectations and
+    get_state unpack, a non-Hermiticity-preserving op mid-plan unpacks inside a CUDA graph,
+    and graph replays recapture when the starting layout differs."""
+    from paper_2404_13184_b200.tanq import Plan
+    rng = np.random.default_rng(77)
+    n = 7
+    c, nm = W.config_workload(3, n=n, depth=4)
+    S = W.random_complex(rng, (16, 16)) * 0.2            # not Hermiticity-preserving
+    c_bad = W.Circuit(n, c.ops[:25] + [W.Op("superop", (2, 5), mat=S)] + c.ops[25:])
+    ref, ref_bad = dense.run(c, nm), dense.run(c_bad, nm)
+    ro = dense.readout_of(nm)
+    with Sim(n) as sim:
+        # herm plan: probabilities (diagonal) straight from the packed layout, then an XY term
+        sim.run_circuit(c, nm)
+        np.testing.assert_allclose(sim.probs(ro), dense.probs(ref, n, ro), atol=ABS)
+        for xm, zm in ((0b0000011, 0b0000001), (0b1010000, 0), (0, 0b1100110)):
+            assert abs(sim.expect_pauli(xm, zm) - dense.expect_pauli(ref, n, xm, zm)) < ABS
+        # continue from the (now unpacked) state with more packed ops, then read everything
+        sim.run_circuit(c, nm)
+        ref2 = dense.run(c, nm, rho=np.ascontiguousarray(ref.copy()))
+        assert sim.check_hermitian()
+        assert_parity(rho_of(sim, n), ref2)
+        # graph replays of a plan whose middle op is not Hermiticity-preserving
+        plan = Plan(sim, c_bad, nm, fuse=2, k_max=3, graph=True)
+        for _ in range(3):                              # (rho is no longer Hermitian: its
+            sim.reset()                                 #  diagonal has an imaginary part, so
+            plan.exec(sim)                              #  compare the full state)
+            assert_parity(rho_of(sim, n), ref_bad)
+        with pytest.raises(Exception):
+            sim.probs()                                 # E_STATE: |Im diag| >= 1e-6
+        # a Hermitian plan replayed from a packed start and from an unpacked start
+        plan2 = Plan(sim, c, nm, fuse=2, k_max=3, graph=True)
+        sim.reset()
+        plan2.exec(sim)                                 # ends packed
+        plan2.exec(sim)                                 # starts packed
+        assert_parity(rho_of(sim, n), ref2)             # get_state unpacks
+        plan2.exec(sim)                                 # starts unpacked: recapture
+        ref3 = dense.run(c, nm, rho=np.ascontiguousarray(ref2.copy()))
+        assert_parity(rho_of(sim, n), ref3)

@@ -1686,6 +1686,12 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   tanq_plan* p = new tanq_plan();
   p->n = n;
   p->ops = fuse(ops, opts.fuse, opts.k_max);
+  if (const char* e = std::getenv("TANQ_PLAN_DUMP"); e && e[0] == '1') {  // diagnostics
+    for (const auto& f : p->ops) {
+      std::fprintf(stderr, "op k=%d subs=%zu q=", f.k, f.sub.size());
+      for (int j = 0; j < f.k; ++j) std::fprintf(stderr, "%d%s", f.q[j], j + 1 < f.k ? "," : "\n");
+    }
+  }
   p->ops_in = c->n_ops;
   p->flags = opts.flags;
   p->plan_ms =

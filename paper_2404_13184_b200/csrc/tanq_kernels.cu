@@ -463,20 +463,27 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
   for (int ks = 0; ks < 4; ++ks) mb[ks] = mi[4 * ks + c4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) md[mt] = mi[8 * mt + r4];
+  // B column of this lane in n-tile j: (sub-tuple member offset, tuple) = (col >> TB, col % T)
+  int mob[4], tb[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if constexpr (T == 8) {  // col >> 3 = n-tile, col & 7 = r4
+      mob[j] = mu[j];
+      tb[j] = r4;
+    } else {
+      const int col = j * 8 + r4;
+      mob[j] = mu[col >> TB];
+      tb[j] = col & (T - 1);
+    }
+  }
+  // The n-tile passes touch disjoint columns (tile elements), and every mma.sync converges the
+  // warp after its B loads, so passes need no __syncwarp between them: the first k-step of
+  // the next pass is loaded before this pass's epilogue, overlapping it with the DMMA tail.
+  double2 xn[UI];
+#pragma unroll
+  for (int u = 0; u < UI; ++u) xn[u] = X[xs_idx<T>(mb[0] | mob[u], tb[u])];
 #pragma unroll
   for (int n0 = 0; n0 < 4; n0 += UI) {
-    int mob[UI], tb[UI];  // B column of this lane in n-tile n0+u: (u, t) = (col >> TB, col % T)
-#pragma unroll
-    for (int u = 0; u < UI; ++u) {
-      if constexpr (T == 8) {  // col >> 3 = n-tile, col & 7 = r4
-        mob[u] = mu[n0 + u];
-        tb[u] = r4;
-      } else {
-        const int col = (n0 + u) * 8 + r4;
-        mob[u] = mu[col >> TB];
-        tb[u] = col & (T - 1);
-      }
-    }
     double p1[UI][2][2], p2[UI][2][2], p3[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
@@ -487,7 +494,12 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
     for (int ks = 0; ks < 4; ++ks) {
       double2 xb[UI];
 #pragma unroll
-      for (int u = 0; u < UI; ++u) xb[u] = X[xs_idx<T>(mb[ks] | mob[u], tb[u])];
+      for (int u = 0; u < UI; ++u)
+        xb[u] = ks == 0 ? xn[u] : X[xs_idx<T>(mb[ks] | mob[n0 + u], tb[n0 + u])];
+      if (ks == 3 && n0 + UI < 4) {
+#pragma unroll
+        for (int u = 0; u < UI; ++u) xn[u] = X[xs_idx<T>(mb[0] | mob[n0 + UI + u], tb[n0 + UI + u])];
+      }
 #pragma unroll
       for (int u = 0; u < UI; ++u) {
         const double xs = xb[u].x + xb[u].y;
@@ -499,20 +511,19 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
         }
       }
     }
-    __syncwarp();
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int col = (n0 + u) * 8 + 2 * c4 + c;
-        const int mo = T == 8 ? mob[u] : mu[col >> TB], t = col & (T - 1);
+        const int mo = T == 8 ? mob[n0 + u] : mu[col >> TB], t = col & (T - 1);
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
           X[xs_idx<T>(md[mt] | mo, t)] = make_double2(
               p1[u][mt][c] - p2[u][mt][c], p3[u][mt][c] - p1[u][mt][c] - p2[u][mt][c]);
       }
-    __syncwarp();
   }
+  __syncwarp();
 }
 
 template <int T>

@@ -820,9 +820,14 @@ bool k2_tiled(const tanq_sim* s, const FusedOp& op) {
   }
   if (op.k != 2 || mode == 0) return false;
   if (mode == 1) return true;
-  int lo = 64;
-  for (int j = 0; j < 2; ++j)
+  int lo = 64, hi = 0;
+  for (int j = 0; j < 2; ++j) {
     lo = std::min(lo, (int)std::min(s->phys[2 * op.q[j]], s->phys[2 * op.q[j] + 1]));
+    hi = std::max(hi, (int)std::max(s->phys[2 * op.q[j]], s->phys[2 * op.q[j] + 1]));
+  }
+  // packed layout: the register stream keeps its in-place fast path only when every target is
+  // low (a high target makes every element's placement depend on the member bits)
+  if (use_mirror(s, op)) return hi >= 6;
   return lo >= 6;
 }
 

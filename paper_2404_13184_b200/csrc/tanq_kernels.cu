@@ -1003,6 +1003,10 @@ cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
   }
   if (p.nq == 2 && mode == 0) mode = 1;
   if (p.mirror && mode == 1) mode = 2;  // packed mode needs whole transpose blocks per tile
+  // packed k=2 tiles: 2-warp CTAs (64 tuples, an even number of tuple bits) -- many small
+  // independent CTAs per SM hide the copy latency best (14.6-15.0 vs 16.8-17.3 ms for 8-warp
+  // tiles at n = 16)
+  if (p.nq == 2 && p.mirror) return launch_tile_cfg<2, 2, 1, 2>(a, p, st);
   switch (mode) {
     case 0:
       if (p.nq == 4) return launch_group_cfg<4, 16, 1, false, 1>(a, p, st);

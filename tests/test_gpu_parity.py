@@ -274,7 +274,7 @@ def _group_circuit(rng, n, qs3, with_dense):
 
 
 @pytest.mark.parametrize("n,qs3", [(3, (0, 1, 2)), (4, (3, 0, 2)), (6, (5, 1, 3)), (8, (0, 7, 4)),
-                                   (9, (8, 6, 7))])
+                                   (9, (8, 6, 7)), (9, (3, 5, 7)), (10, (1, 4, 6))])
 @pytest.mark.parametrize("with_dense", [False, True])
 def test_group_programs(Sim, n, qs3, with_dense):
     from paper_2404_13184_b200.tanq import Plan

@@ -57,11 +57,11 @@ NcclApi& nccl() {
   static bool tried = false;
   if (tried) return api;
   tried = true;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!h) {
-    const char* env = getenv("TANQ_NCCL_LIB");
-    h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  }
+  // TANQ_NCCL_LIB names another implementation of the NCCL calls used here (tests: the
+  // host-staged transport of tests/nccl_shim.cpp, which lets several ranks share one GPU)
+  const char* env = getenv("TANQ_NCCL_LIB");
+  void* h = env ? dlopen(env, RTLD_NOW | RTLD_LOCAL) : dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h && !env) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) return api;
 #define LOAD(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
   LOAD(GetUniqueId);

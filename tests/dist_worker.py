@@ -1,0 +1,55 @@
+"""Worker for tests/test_gpu_dist.py (not a test module): one rank of the multi-process path
+(tanq_create_dist) on a random noisy circuit whose top qubits are global, checked against the
+CPU oracle on rank 0.  Launched with torch.distributed.run; the NCCL calls of libtanq go to
+TANQ_NCCL_LIB (the host-staged shim when all ranks share one GPU)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--qubits", type=int, default=6)
+    ap.add_argument("--seed", type=int, default=5)
+    ap.add_argument("--depth", type=int, default=60)
+    args = ap.parse_args()
+    import numpy as np
+    import torch.distributed as dist
+    import workloads as W
+    from paper_2404_13184_b200 import Simulator, nccl_unique_id
+
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    dist.init_process_group("gloo")  # bootstrap of the unique id only
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    n = args.qubits
+    c = W.random_circuit(n, args.depth, seed=args.seed, kmax=3)
+    nm = W.synthetic_calibration(c, args.seed, depol=True, thermal=True, overrot=True)
+    xm, zm = 0b11 << (n - 2), 0b101 << (n - 3)      # touches the global qubits
+    with Simulator(n, world_size=world, rank=rank, device=0, nccl_uid=uid[0]) as sim:
+        st = sim.run_circuit(c, nm, fuse=2, k_max=3)
+        vec = sim.get_state()                        # whole vec(rho), all-reduced
+        p = sim.probs()
+        z = sim.expect_pauli(xm, zm)
+    if rank == 0:
+        from oracle import dense
+        ref = dense.run(c, nm)
+        N = 2 ** n
+        got = vec.reshape(N, N).T
+        err = float(np.abs(got - ref).max())
+        rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+        perr = float(np.abs(p - np.diag(ref).real).max())
+        zerr = abs(z - dense.expect_pauli(ref, n, xm, zm))
+        ok = err <= 1e-10 and rel <= 1e-12 and perr <= 1e-10 and zerr <= 1e-10 and st["n_remaps"] > 0
+        print(f"DIST world={world} n={n} remaps={st['n_remaps']} max_abs={err:.3e} rel={rel:.3e} "
+              f"probs={perr:.3e} expect={zerr:.3e} {'OK' if ok else 'MISMATCH'}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0 and not ok:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()

@@ -194,10 +194,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # TANQ_NCCL_LIB = the NCCL test shim (tests/nccl_shim): ranks may share one GPU, the
+    # torch-level plumbing runs on gloo; a functional check of the N > 1 path, not a timing
+    shim = bool(os.environ.get("TANQ_NCCL_LIB"))
+    dev = local % torch.cuda.device_count() if shim else local
+    torch.cuda.set_device(dev)
+    tdev = "cpu" if shim else "cuda"
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shim:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from __graft_entry__ import build
     if rank == 0:
@@ -213,9 +221,9 @@ def run_ours(args):
     if world > 1:
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        sim = Simulator(n, world_size=world, rank=rank, device=local, nccl_uid=uid[0])
+        sim = Simulator(n, world_size=world, rank=rank, device=dev, nccl_uid=uid[0])
     elif "WORLD_SIZE" in os.environ and args.shards == 1:  # torchrun N=1: the per-rank API
-        sim = Simulator(n, world_size=1, rank=0, device=local)
+        sim = Simulator(n, world_size=1, rank=0, device=dev)
     else:
         sim = Simulator(n, args.shards)
     stream = torch.cuda.Stream()          # a real stream: events on it bracket the kernels
@@ -236,7 +244,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev)
     clk.start()
     l0 = sim.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -252,7 +260,7 @@ def run_ours(args):
     launches = sim.launch_count() - l0
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -311,7 +319,7 @@ def run_ours(args):
         t_e2e.append(time.perf_counter() - a0)
     e2e_s = statistics.median(t_e2e)
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = plan.h2d_bytes + sum(16 * (16 ** k) * st2[f"n_k{k}"] for k in (1, 2, 3))
@@ -335,7 +343,9 @@ def run_ours(args):
                        "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
                        "remaps_per_step": st["n_remaps"],
                        "state_bytes": 16 * 4 ** n, "shard_bytes": info["shard_bytes"],
-                       "parallelism": (f"state partitioned over {world} GPU(s) by high bits"
+                       "parallelism": (f"{world} ranks sharing GPU(s) through the NCCL test shim "
+                                       f"(functional check, not a timing)" if shim and world > 1 else
+                                       f"state partitioned over {world} GPU(s) by high bits"
                                        if args.shards == 1 else
                                        f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
                        "l2": "inputs larger than L2 (state >> 126 MB)" if 16 * 4 ** n > 5e8
@@ -370,7 +380,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=None,
+                    help="qubits of the workload (--qubits under torchrun: it claims --n)")
     ap.add_argument("--fuse", type=int, default=2)
     ap.add_argument("--kmax", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=15.0)

@@ -671,6 +671,70 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
   return TANQ_OK;
 }
 
+bool batch_remaps() {  // env TANQ_REMAP_BATCH=0: two pairwise exchanges instead
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TANQ_REMAP_BATCH");
+    v = e && e[0] == '0' ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Two swaps (a0 <-> b0, a1 <-> b1; a0 != a1 global, b0 != b1 local) as ONE exchange in the
+// multi-process mode: after both swaps an element with local bits (l0, l1) at
+// (b0, b1) lives on the shard whose bits (a0, a1) are (l0, l1), at local bits (b0, b1) = this
+// shard's (g0, g1).  So the quarter with (l0, l1) = (g0, g1) stays, and for each of the 3
+// peers h: this shard's quarter (l0, l1) = (h0, h1) goes to h and h's quarter (g0, g1) lands in
+// its place.  3/4 of the shard crosses NVLink instead of 2 x 1/2 for two pairwise swaps; the
+// result is identical to the two swaps in sequence (same bit map).
+tanq_status remap_swap2(tanq_sim* s, int a0, int b0, int a1, int b1) {
+  if (!s->dist || a0 == a1 || b0 == b1) {
+    TRY(remap_swap(s, a0, b0));
+    return remap_swap(s, a1, b1);
+  }
+  TRY(ensure_unpacked(s));
+  const int L = s->L;
+  Shard& sh = s->shards[0];
+  const int g = sh.id, ga0 = a0 - L, ga1 = a1 - L;
+  // order the local bits for the quarter kernels (values travel with their bits)
+  const bool sw = b0 > b1;
+  const int lb0 = sw ? b1 : b0, lb1 = sw ? b0 : b1;
+  const uint64_t quarter = (uint64_t)1 << (L - 2);
+  CUDA_TRY(cudaSetDevice(sh.device));
+  Prof pr{3, nullptr, nullptr, 2.0 * 3.0 * quarter * sizeof(double2), 0.0, 0.0};
+  prof_begin(s, sh, pr);
+  for (int h0 = 0; h0 < 2; ++h0)
+    for (int h1 = 0; h1 < 2; ++h1) {
+      const int peer = (g & ~((1 << ga0) | (1 << ga1))) | (h0 << ga0) | (h1 << ga1);
+      if (peer == g) continue;
+      const int v0 = sw ? h1 : h0, v1 = sw ? h0 : h1;  // bit values at lb0 < lb1
+      for (uint64_t first = 0; first < quarter; first += s->xchunk) {
+        const uint64_t cnt = std::min<uint64_t>(s->xchunk, quarter - first);
+        CUDA_TRY(tanq::launch_pack_quarter(sh.data, s->xsend, lb0, v0, lb1, v1, first, cnt,
+                                           sh.stream));
+        NCCL_TRY(nccl().GroupStart());
+        NCCL_TRY(nccl().Send(s->xsend, cnt * 2, ncclDouble, peer, s->comm, sh.stream));
+        NCCL_TRY(nccl().Recv(s->xrecv, cnt * 2, ncclDouble, peer, s->comm, sh.stream));
+        NCCL_TRY(nccl().GroupEnd());
+        CUDA_TRY(tanq::launch_unpack_quarter(sh.data, s->xrecv, lb0, v0, lb1, v1, first, cnt,
+                                             sh.stream));
+        s->launches += 2;
+        s->remap_bytes += cnt * sizeof(double2);
+      }
+    }
+  prof_end(s, sh, pr);
+  for (auto [a, b] : {std::pair<int, int>{a0, b0}, std::pair<int, int>{a1, b1}}) {
+    for (int i = 0; i < 2 * s->n; ++i) {
+      if (s->phys[i] == (uint32_t)a)
+        s->phys[i] = (uint32_t)b;
+      else if (s->phys[i] == (uint32_t)b)
+        s->phys[i] = (uint32_t)a;
+    }
+    s->remap_count++;
+  }
+  return TANQ_OK;
+}
+
 // Victim for a remap (pure layout logic, shared by execution and tanq_plan_schedule): a local
 // bit not targeted by the op whose qubit is used furthest in the future (lookahead 256 ops
 // over `next` from `next_from`), ties to the highest position.  -1 if none.
@@ -735,10 +799,14 @@ tanq_status ensure_local(tanq_sim* s, const FusedOp& op, const std::vector<Fused
   uint32_t phys[64];
   std::memcpy(phys, s->phys, sizeof(phys));
   auto swaps = plan_remaps(phys, s->n, s->L, op, next, next_from);
-  for (auto& ab : swaps) {
+  for (auto& ab : swaps)
     if (ab.first < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
-    TRY(remap_swap(s, ab.first, ab.second));
-  }
+  // swaps are independent (distinct global and distinct local bits): batch them in pairs
+  size_t i = 0;
+  if (s->dist && batch_remaps())
+    for (; i + 1 < swaps.size(); i += 2)
+      TRY(remap_swap2(s, swaps[i].first, swaps[i].second, swaps[i + 1].first, swaps[i + 1].second));
+  for (; i < swaps.size(); ++i) TRY(remap_swap(s, swaps[i].first, swaps[i].second));
   return TANQ_OK;
 }
 

@@ -74,6 +74,11 @@ cudaError_t launch_pack_half(const double2* a, double2* buf, int b, int v, uint6
                              uint64_t count, cudaStream_t st);
 cudaError_t launch_unpack_half(double2* a, const double2* buf, int b, int v, uint64_t first,
                                uint64_t count, cudaStream_t st);
+// the same for the quarter {o : bit_b0(o) == v0, bit_b1(o) == v1}, b0 < b1
+cudaError_t launch_pack_quarter(const double2* a, double2* buf, int b0, int v0, int b1, int v1,
+                                uint64_t first, uint64_t count, cudaStream_t st);
+cudaError_t launch_unpack_quarter(double2* a, const double2* buf, int b0, int v0, int b1, int v1,
+                                  uint64_t first, uint64_t count, cudaStream_t st);
 
 // Paper vec index v = r + c 2^n  <->  physical index; gather / scatter the owned entries
 // of a range [first, first+count) of vec(rho) for shard `shard` (local bits L).

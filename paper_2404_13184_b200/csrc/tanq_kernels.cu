@@ -1098,6 +1098,37 @@ cudaError_t launch_unpack_half(double2* a, const double2* buf, int b, int v, uin
   return cudaGetLastError();
 }
 
+// Quarter {o : bit_b0(o) == v0, bit_b1(o) == v1} (b0 < b1) of a shard to / from a contiguous
+// buffer, elements [first, first + count) of the quarter in run order (batched 2-bit remap).
+__global__ void pack_quarter_kernel(double2* __restrict__ a, double2* __restrict__ buf, int b0,
+                                    int v0, int b1, int v1, uint64_t first, uint64_t count,
+                                    int dir) {
+  const uint64_t m0 = ((uint64_t)1 << b0) - 1, m1 = ((uint64_t)1 << b1) - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    uint64_t o = first + i;
+    o = ((o & ~m0) << 1) | ((uint64_t)v0 << b0) | (o & m0);
+    o = ((o & ~m1) << 1) | ((uint64_t)v1 << b1) | (o & m1);
+    if (dir == 0)
+      buf[i] = a[o];
+    else
+      a[o] = buf[i];
+  }
+}
+
+cudaError_t launch_pack_quarter(const double2* a, double2* buf, int b0, int v0, int b1, int v1,
+                                uint64_t first, uint64_t count, cudaStream_t st) {
+  pack_quarter_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      const_cast<double2*>(a), buf, b0, v0, b1, v1, first, count, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack_quarter(double2* a, const double2* buf, int b0, int v0, int b1, int v1,
+                                  uint64_t first, uint64_t count, cudaStream_t st) {
+  pack_quarter_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, const_cast<double2*>(buf), b0, v0, b1, v1, first, count, 1);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------
 // vec(rho) order <-> physical order
 // ------------------------------------------------------------------------------------

@@ -43,7 +43,7 @@ def main():
         perr = float(np.abs(p - np.diag(ref).real).max())
         zerr = abs(z - dense.expect_pauli(ref, n, xm, zm))
         ok = err <= 1e-10 and rel <= 1e-12 and perr <= 1e-10 and zerr <= 1e-10 and st["n_remaps"] > 0
-        print(f"DIST world={world} n={n} remaps={st['n_remaps']} max_abs={err:.3e} rel={rel:.3e} "
+        print(f"DIST world={world} n={n} remaps={st['n_remaps']} remap_bytes={st['remap_bytes']} max_abs={err:.3e} rel={rel:.3e} "
               f"probs={perr:.3e} expect={zerr:.3e} {'OK' if ok else 'MISMATCH'}", flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -52,3 +52,22 @@ def test_dist_remap_parity(shim, world, n, seed, batch):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("DIST")]
     assert line and line[-1].endswith("OK"), out[-4000:]
     print(line[-1])
+
+
+@pytest.mark.parametrize("world,config,n", [(8, 5, 8), (4, 4, 7)])
+def test_dist_config_workloads(shim, world, config, n):
+    """BASELINE configs 5 (VQE ansatz + its Pauli-string Hamiltonian, the 8-GPU config) and 4
+    (QPE with calibrated noise + readout) scaled down, on `world` ranks: state, readout-noisy
+    probabilities and every Pauli expectation against the oracle."""
+    env = dict(os.environ, TANQ_NCCL_LIB=shim, OMP_NUM_THREADS="2")
+    port = 29800 + 10 * world + config
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+                        "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), os.path.join(ROOT, "tests", "dist_worker.py"),
+                        "--qubits", str(n), "--config", str(config)],
+                       env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("DIST")]
+    assert line and line[-1].endswith("OK"), out[-4000:]
+    print(line[-1])

@@ -503,9 +503,11 @@ struct tanq_sim {
   std::vector<DevScratch> scratch;  // per distinct device
   uint32_t phys[64];                // logical bit (2q row, 2q+1 col) -> physical bit
   ncclComm_t comm = nullptr;
-  double2* xsend = nullptr;
-  double2* xrecv = nullptr;
+  double2* xsend = nullptr;         // 2 staging slots of xchunk elements (send)
+  double2* xrecv = nullptr;         // 2 staging slots (receive)
   size_t xchunk = 0;
+  cudaStream_t xstream = nullptr;   // NCCL stream of the pipelined exchange
+  cudaEvent_t xev_pack[2] = {nullptr, nullptr}, xev_comm[2] = {nullptr, nullptr};
   bool prof_on = false;
   std::vector<Prof> prof;
   std::vector<cudaEvent_t> event_pool;  // recycled timing events (no create per launch)
@@ -615,6 +617,45 @@ void prof_end(tanq_sim* s, Shard& sh, Prof& p) {
 // Swap physical bit a (global, a >= L) with local bit b (A-6).
 tanq_status ensure_unpacked(tanq_sim* s);
 
+// Chunked exchange of `total` elements with `peer` through 2 x 2 staging slots, pipelined
+// (SURVEY NEXT-2 overlap): pack / unpack kernels run on the shard's stream, the grouped
+// send/recv on s->xstream, so chunk i's transfer overlaps chunk i-1's unpack and chunk i+1's
+// pack.  Stream S: pack0 pack1 | unpack0 pack2 | unpack1 pack3 ...; stream X: comm0 comm1 ...
+// Ordering: comm(i) waits pack(i) (event xev_pack[j]); unpack(i) waits comm(i) (xev_comm[j]);
+// pack(i+2) reuses slot j after unpack(i) on S, so slot reuse is ordered by S itself.
+// In place: pack(i) reads chunk i of the outgoing part before unpack(i) overwrites it (S order).
+template <class Pack, class Unpack>
+tanq_status exchange_pipelined(tanq_sim* s, Shard& sh, int peer, uint64_t total, Pack pack,
+                               Unpack unpack) {
+  const uint64_t C = s->xchunk, nch = (total + C - 1) / C;
+  auto cnt_of = [&](uint64_t i) { return std::min<uint64_t>(C, total - i * C); };
+  for (uint64_t i = 0; i < std::min<uint64_t>(2, nch); ++i) {
+    CUDA_TRY(pack(i * C, cnt_of(i), s->xsend + (i & 1) * C));
+    CUDA_TRY(cudaEventRecord(s->xev_pack[i & 1], sh.stream));
+    s->launches++;
+  }
+  for (uint64_t i = 0; i < nch; ++i) {
+    const int j = (int)(i & 1);
+    const uint64_t cnt = cnt_of(i);
+    CUDA_TRY(cudaStreamWaitEvent(s->xstream, s->xev_pack[j], 0));
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().Send(s->xsend + j * C, cnt * 2, ncclDouble, peer, s->comm, s->xstream));
+    NCCL_TRY(nccl().Recv(s->xrecv + j * C, cnt * 2, ncclDouble, peer, s->comm, s->xstream));
+    NCCL_TRY(nccl().GroupEnd());
+    CUDA_TRY(cudaEventRecord(s->xev_comm[j], s->xstream));
+    CUDA_TRY(cudaStreamWaitEvent(sh.stream, s->xev_comm[j], 0));
+    CUDA_TRY(unpack(i * C, cnt, s->xrecv + j * C));
+    s->launches++;
+    if (i + 2 < nch) {
+      CUDA_TRY(pack((i + 2) * C, cnt_of(i + 2), s->xsend + j * C));
+      CUDA_TRY(cudaEventRecord(s->xev_pack[j], sh.stream));
+      s->launches++;
+    }
+    s->remap_bytes += cnt * sizeof(double2);
+  }
+  return TANQ_OK;
+}
+
 tanq_status remap_swap(tanq_sim* s, int a, int b) {
   TRY(ensure_unpacked(s));  // (packed mode is single-shard only; kept for safety)
   const int L = s->L, gb = a - L;
@@ -647,17 +688,14 @@ tanq_status remap_swap(tanq_sim* s, int a, int b) {
     // bytes = the half sent + the half received over NVLink
     Prof pr{3, nullptr, nullptr, 2.0 * half * sizeof(double2), 0.0, 0.0};
     prof_begin(s, sh, pr);
-    for (uint64_t first = 0; first < half; first += s->xchunk) {
-      const uint64_t cnt = std::min<uint64_t>(s->xchunk, half - first);
-      CUDA_TRY(tanq::launch_pack_half(sh.data, s->xsend, b, v, first, cnt, sh.stream));
-      NCCL_TRY(nccl().GroupStart());
-      NCCL_TRY(nccl().Send(s->xsend, cnt * 2, ncclDouble, g2, s->comm, sh.stream));
-      NCCL_TRY(nccl().Recv(s->xrecv, cnt * 2, ncclDouble, g2, s->comm, sh.stream));
-      NCCL_TRY(nccl().GroupEnd());
-      CUDA_TRY(tanq::launch_unpack_half(sh.data, s->xrecv, b, v, first, cnt, sh.stream));
-      s->launches += 2;
-      s->remap_bytes += cnt * sizeof(double2);
-    }
+    TRY(exchange_pipelined(
+        s, sh, g2, half,
+        [&](uint64_t first, uint64_t cnt, double2* buf) {
+          return tanq::launch_pack_half(sh.data, buf, b, v, first, cnt, sh.stream);
+        },
+        [&](uint64_t first, uint64_t cnt, const double2* buf) {
+          return tanq::launch_unpack_half(sh.data, buf, b, v, first, cnt, sh.stream);
+        }));
     prof_end(s, sh, pr);
   }
   // bookkeeping: logical bits at a and b exchange positions
@@ -708,19 +746,15 @@ tanq_status remap_swap2(tanq_sim* s, int a0, int b0, int a1, int b1) {
       const int peer = (g & ~((1 << ga0) | (1 << ga1))) | (h0 << ga0) | (h1 << ga1);
       if (peer == g) continue;
       const int v0 = sw ? h1 : h0, v1 = sw ? h0 : h1;  // bit values at lb0 < lb1
-      for (uint64_t first = 0; first < quarter; first += s->xchunk) {
-        const uint64_t cnt = std::min<uint64_t>(s->xchunk, quarter - first);
-        CUDA_TRY(tanq::launch_pack_quarter(sh.data, s->xsend, lb0, v0, lb1, v1, first, cnt,
-                                           sh.stream));
-        NCCL_TRY(nccl().GroupStart());
-        NCCL_TRY(nccl().Send(s->xsend, cnt * 2, ncclDouble, peer, s->comm, sh.stream));
-        NCCL_TRY(nccl().Recv(s->xrecv, cnt * 2, ncclDouble, peer, s->comm, sh.stream));
-        NCCL_TRY(nccl().GroupEnd());
-        CUDA_TRY(tanq::launch_unpack_quarter(sh.data, s->xrecv, lb0, v0, lb1, v1, first, cnt,
-                                             sh.stream));
-        s->launches += 2;
-        s->remap_bytes += cnt * sizeof(double2);
-      }
+      TRY(exchange_pipelined(
+          s, sh, peer, quarter,
+          [&](uint64_t first, uint64_t cnt, double2* buf) {
+            return tanq::launch_pack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt, sh.stream);
+          },
+          [&](uint64_t first, uint64_t cnt, const double2* buf) {
+            return tanq::launch_unpack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt,
+                                               sh.stream);
+          }));
     }
   prof_end(s, sh, pr);
   for (auto [a, b] : {std::pair<int, int>{a0, b0}, std::pair<int, int>{a1, b1}}) {
@@ -1343,7 +1377,7 @@ static tanq_status create_common(int n, tanq_sim* s) {
     int same = 0;
     for (auto& o : s->shards) same += (o.device == sh.device && o.data == nullptr);
     const size_t need = shard_bytes * (size_t)same + ((size_t)64 << 20) +
-                        (s->dist ? 2 * s->xchunk * sizeof(double2) : 0) + (sizeof(double) * 3 << n);
+                        (s->dist ? 4 * s->xchunk * sizeof(double2) : 0) + (sizeof(double) * 3 << n);
     if (need > fr)
       return fail(TANQ_E_NOMEM, "memory guard: need " + std::to_string(need) + " B, free " +
                                     std::to_string(fr) + " B on device " +
@@ -1451,13 +1485,22 @@ tanq_status tanq_create_dist(int n_qubits, int world_size, int rank, int device,
   sh.id = rank;
   sh.device = device;
   s->shards.push_back(sh);
-  s->xchunk = std::min<size_t>((size_t)1 << 24, (size_t)1 << (L > 1 ? L - 1 : 0));  // 256 MiB
+  // 2 x 2 staging slots of 128 MiB (pipelined exchange); env TANQ_XCHUNK_LOG2 (tests) caps
+  // a slot at 2^k elements so small states still run several chunks
+  int xlog = 23;
+  if (const char* e = std::getenv("TANQ_XCHUNK_LOG2")) xlog = std::max(4, std::min(23, std::atoi(e)));
+  s->xchunk = std::min<size_t>((size_t)1 << xlog, (size_t)1 << (L > 2 ? L - 2 : 0));
   tanq_status st = create_common(n_qubits, s);
   if (st == TANQ_OK && world_size > 1) {
     cudaSetDevice(device);
-    if (cudaMalloc(&s->xsend, s->xchunk * sizeof(double2)) != cudaSuccess ||
-        cudaMalloc(&s->xrecv, s->xchunk * sizeof(double2)) != cudaSuccess)
+    if (cudaMalloc(&s->xsend, 2 * s->xchunk * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&s->xrecv, 2 * s->xchunk * sizeof(double2)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking) != cudaSuccess)
       st = fail(TANQ_E_NOMEM, "staging");
+    for (int j = 0; j < 2 && st == TANQ_OK; ++j)
+      if (cudaEventCreateWithFlags(&s->xev_pack[j], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s->xev_comm[j], cudaEventDisableTiming) != cudaSuccess)
+        st = fail(TANQ_E_CUDA, "exchange events");
     ncclUniqueId id;
     std::memcpy(&id, nccl_uid, sizeof(id));
     if (st == TANQ_OK) {
@@ -1508,6 +1551,11 @@ tanq_status tanq_destroy(tanq_sim* s) {
   if (s->frag_done) cudaEventDestroy(s->frag_done);
   if (s->xsend) cudaFree(s->xsend);
   if (s->xrecv) cudaFree(s->xrecv);
+  if (s->xstream) cudaStreamDestroy(s->xstream);
+  for (int j = 0; j < 2; ++j) {
+    if (s->xev_pack[j]) cudaEventDestroy(s->xev_pack[j]);
+    if (s->xev_comm[j]) cudaEventDestroy(s->xev_comm[j]);
+  }
   if (s->comm) nccl().CommDestroy(s->comm);
   cudaGetLastError();
   delete s;

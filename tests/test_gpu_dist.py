@@ -35,13 +35,17 @@ def shim(tmp_path_factory):
     return out
 
 
-@pytest.mark.parametrize("world,n,seed,batch", [(2, 6, 5, "1"), (2, 7, 6, "1"), (4, 6, 7, "1"),
-                                                (8, 6, 8, "1"), (4, 7, 9, "1"), (4, 6, 7, "0"),
-                                                (8, 6, 8, "0")])
-def test_dist_remap_parity(shim, world, n, seed, batch):
-    """batch = 1: two swaps of one op run as one 4-way exchange (remap_swap2); 0: pairwise."""
-    env = dict(os.environ, TANQ_NCCL_LIB=shim, OMP_NUM_THREADS="2", TANQ_REMAP_BATCH=batch)
-    port = 29600 + 10 * world + n + 100 * int(batch)
+@pytest.mark.parametrize("world,n,seed,batch,xlog", [
+    (2, 6, 5, "1", "23"), (2, 7, 6, "1", "23"), (4, 6, 7, "1", "23"), (8, 6, 8, "1", "23"),
+    (4, 7, 9, "1", "23"), (4, 6, 7, "0", "23"), (8, 6, 8, "0", "23"),
+    (2, 7, 6, "1", "5"), (4, 7, 9, "1", "6"), (8, 6, 8, "0", "4")])
+def test_dist_remap_parity(shim, world, n, seed, batch, xlog):
+    """batch = 1: two swaps of one op run as one 4-way exchange (remap_swap2); 0: pairwise.
+    xlog: staging slot of 2^xlog amplitudes -- small slots run the pipelined exchange over
+    many chunks (comm on its own stream, pack / unpack overlapped)."""
+    env = dict(os.environ, TANQ_NCCL_LIB=shim, OMP_NUM_THREADS="2", TANQ_REMAP_BATCH=batch,
+               TANQ_XCHUNK_LOG2=xlog)
+    port = 29600 + 10 * world + n + 100 * int(batch) + int(xlog)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
                         "--nproc-per-node", str(world), "--master-addr", "127.0.0.1",
                         "--master-port", str(port), os.path.join(ROOT, "tests", "dist_worker.py"),

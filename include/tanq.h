@@ -127,8 +127,9 @@ typedef struct {
  * with the B200 cost model (default).  k_max in {1,2,3,4}: fused superoperators never exceed
  * 2 qubits (or a user's 3-qubit op); k_max >= 3 lets the K3 group kernel run several of them
  * in one HBM pass over 3-qubit (k_max = 3, default) or up to 4-qubit tiles (k_max = 4; slower
- * at n = 16 on B200).  chunk_bytes: remap staging chunk
- * (0 = default 256 MiB).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
+ * at n = 16 on B200).  chunk_bytes: reserved, must be 0 (the remap
+ * staging is fixed when a multi-process handle is created: 2 x 2 pipelined slots of 128 MiB,
+ * DESIGN.md §7).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
  * on single-shard handles capture their launches into a CUDA graph on the first
  * tanq_plan_exec and replay it afterwards (ignored with bit0); bit2 = disable the
  * Hermitian mirror mode for this run. */

@@ -741,20 +741,21 @@ tanq_status remap_swap2(tanq_sim* s, int a0, int b0, int a1, int b1) {
   CUDA_TRY(cudaSetDevice(sh.device));
   Prof pr{3, nullptr, nullptr, 2.0 * 3.0 * quarter * sizeof(double2), 0.0, 0.0};
   prof_begin(s, sh, pr);
-  for (int h0 = 0; h0 < 2; ++h0)
-    for (int h1 = 0; h1 < 2; ++h1) {
-      const int peer = (g & ~((1 << ga0) | (1 << ga1))) | (h0 << ga0) | (h1 << ga1);
-      if (peer == g) continue;
-      const int v0 = sw ? h1 : h0, v1 = sw ? h0 : h1;  // bit values at lb0 < lb1
-      TRY(exchange_pipelined(
-          s, sh, peer, quarter,
-          [&](uint64_t first, uint64_t cnt, double2* buf) {
-            return tanq::launch_pack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt, sh.stream);
-          },
-          [&](uint64_t first, uint64_t cnt, const double2* buf) {
-            return tanq::launch_unpack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt,
-                                               sh.stream);
-          }));
+  // step d pairs every shard with g ^ (d on bits ga0, ga1): mutual partners at every step, so
+  // the grouped send/recv rendezvous cannot form a cycle
+  for (int d = 1; d < 4; ++d) {
+    const int h0 = ((g >> ga0) & 1) ^ (d & 1), h1 = ((g >> ga1) & 1) ^ (d >> 1);
+    const int peer = (g & ~((1 << ga0) | (1 << ga1))) | (h0 << ga0) | (h1 << ga1);
+    const int v0 = sw ? h1 : h0, v1 = sw ? h0 : h1;  // bit values at lb0 < lb1
+    TRY(exchange_pipelined(
+        s, sh, peer, quarter,
+        [&](uint64_t first, uint64_t cnt, double2* buf) {
+          return tanq::launch_pack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt, sh.stream);
+        },
+        [&](uint64_t first, uint64_t cnt, const double2* buf) {
+          return tanq::launch_unpack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt,
+                                             sh.stream);
+        }));
     }
   prof_end(s, sh, pr);
   for (auto [a, b] : {std::pair<int, int>{a0, b0}, std::pair<int, int>{a1, b1}}) {

@@ -756,7 +756,7 @@ tanq_status remap_swap2(tanq_sim* s, int a0, int b0, int a1, int b1) {
           return tanq::launch_unpack_quarter(sh.data, buf, lb0, v0, lb1, v1, first, cnt,
                                              sh.stream);
         }));
-    }
+  }
   prof_end(s, sh, pr);
   for (auto [a, b] : {std::pair<int, int>{a0, b0}, std::pair<int, int>{a1, b1}}) {
     for (int i = 0; i < 2 * s->n; ++i) {

@@ -414,6 +414,43 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
     g.members.push_back(gi);
     groups.push_back(std::move(g));
   }
+  // Forward merge (post-pass): a group may move LATER, past groups disjoint from its qubits,
+  // into the first later group that shares a qubit with it, when their union still fits a
+  // tile.  Its members run first (they precede, or commute with, every member of the target:
+  // a member sharing a qubit with the target would have joined the target, the latest sharing
+  // group).  A k=2 op left standalone because the group before it was full then rides in the
+  // next group's pass instead of costing its own HBM pass.  Env TANQ_FWD_MERGE=0 disables.
+  static int fwd = -1;
+  if (fwd < 0) {
+    const char* e = std::getenv("TANQ_FWD_MERGE");
+    fwd = e && e[0] == '0' ? 0 : 1;
+  }
+  for (size_t i = 0; fwd && i < groups.size(); ++i) {
+    Group& A = groups[i];
+    if (A.members.empty()) continue;
+    for (size_t j = i + 1; j < groups.size(); ++j) {
+      Group& B = groups[j];
+      if (B.members.empty() || !shares(B.op, A.op.q, A.op.k)) continue;
+      bool has3 = false;
+      for (int m : A.members) has3 |= l1[m].k == 3;
+      for (int m : B.members) has3 |= l1[m].k == 3;
+      const int lim = has3 ? 3 : glim;
+      int uq[8], uk = B.op.k;
+      for (int t = 0; t < B.op.k; ++t) uq[t] = B.op.q[t];
+      for (int t = 0; t < A.op.k; ++t) {
+        bool f = false;
+        for (int u = 0; u < uk; ++u) f |= uq[u] == A.op.q[t];
+        if (!f) uq[uk++] = A.op.q[t];
+      }
+      if (uk <= lim && uk >= 3) {  // (k <= 2 unions were already merged by level 1)
+        B.op.k = uk;
+        for (int t = 0; t < uk; ++t) B.op.q[t] = uq[t];
+        B.members.insert(B.members.begin(), A.members.begin(), A.members.end());
+        A.members.clear();
+      }
+      break;  // only the first later group sharing a qubit may absorb A
+    }
+  }
   // the dense superoperator of a group on its union (members applied in order)
   auto dense_of = [&](const Group& g) {
     FusedOp acc = l1[g.members[0]];
@@ -431,6 +468,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   };
   std::vector<FusedOp> out;
   for (Group& g : groups) {
+    if (g.members.empty()) continue;  // moved into a later group
     if (g.members.size() == 1 || g.op.k < 3) {  // k<=2 unions were merged by level 1
       for (int m : g.members) out.push_back(l1[m]);
       continue;

@@ -1849,7 +1849,12 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   if (const char* e = std::getenv("TANQ_PLAN_DUMP"); e && e[0] == '1') {  // diagnostics
     for (const auto& f : p->ops) {
       std::fprintf(stderr, "op k=%d subs=%zu q=", f.k, f.sub.size());
-      for (int j = 0; j < f.k; ++j) std::fprintf(stderr, "%d%s", f.q[j], j + 1 < f.k ? "," : "\n");
+      for (int j = 0; j < f.k; ++j) std::fprintf(stderr, "%d%s", f.q[j], j + 1 < f.k ? "," : "");
+      for (const auto& sb : f.sub) {
+        std::fprintf(stderr, " [");
+        for (int j = 0; j < sb.k; ++j) std::fprintf(stderr, "%d%s", sb.q[j], j + 1 < sb.k ? "," : "]");
+      }
+      std::fprintf(stderr, "\n");
     }
   }
   p->ops_in = c->n_ops;

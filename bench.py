@@ -113,59 +113,126 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # CPU baseline: the oracle as it stands, on a bounded sample of the same workload
 # --------------------------------------------------------------------------------------
-def oracle_sample(config: int, n_full: int, ops_fused: int, budget_s: float = 15.0):
-    import numpy as np
+def plan_counts(config: int, n: int, world: int, fuse: int, kmax: int):
+    """Fused-gate updates per circuit of the GPU plan, from the committed table written by
+    scripts/plan_counts.py (the reference arm must not load libtanq.so to count them)."""
+    p = os.path.join(ROOT, "workloads", "plan_counts.json")
+    key = f"config{config}:n{n}:gpus{world}:fuse{fuse}:kmax{kmax}"
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    if key not in d:
+        raise SystemExit(f"no plan count for {key}: run scripts/plan_counts.py")
+    return d[key]
+
+
+def gate_classes(circ, nm):
+    """Basis gates grouped by their oracle channel sequence (kind, arity, channel kinds)."""
+    from oracle import channels
+    out = {}
+    for op in circ.ops:
+        seq = channels.gate_channel_sequence(op, nm)
+        key = (op.kind, len(op.qubits), tuple((k, len(q)) for k, q, _ in seq))
+        out.setdefault(key, []).append(op)
+    return out
+
+
+def oracle_estimate(config: int, n_full: int, gate_updates: int, budget_s: float = 8.0,
+                    n_sample: int = 13):
+    """Oracle seconds per whole n_full circuit from a bounded, representative sample: every
+    basis gate of the circuit belongs to one of a few channel-sequence classes (e.g. config 4:
+    RZ = 1 Kraus channel; SX/X = U, AD, PD, 1q depolarizing; CX = U, 4 thermal, 2q
+    depolarizing); one instance of each class is timed on the oracle at n_sample (<= n_full)
+    qubits, repeated round-robin while the budget lasts, and the circuit time is
+    sum_class count(class) x mean time(class) x 4^(n_full - n_sample) (the oracle's per-gate
+    work is O(4^n): every block of the dense rho).  value = the GPU plan's fused-gate updates
+    per circuit / that time."""
     import workloads as W
     from oracle import channels, dense
 
-    n_s = min(n_full, 13 if n_full > 14 else n_full)
-    c_full, _ = W.config_workload(config, n=n_full)
-    c, nm = W.config_workload(config, n=n_s)
+    n_s = min(n_full, n_sample)
+    c_full, nm_full = W.config_workload(config, n=n_full)
+    c_s, nm_s = W.config_workload(config, n=n_s)
+    full_cls = gate_classes(c_full, nm_full)
+    samp_cls = gate_classes(c_s, nm_s)
+    missing = [k for k in full_cls if k not in samp_cls]
+    if missing:
+        raise RuntimeError(f"gate classes {missing} absent at n={n_s}")
     rho = dense.ground(n_s)
     dense.lib()
+    first = next(iter(samp_cls.values()))[0]        # untimed: OpenMP pool + page warm-up
+    dense.apply_channel_seq(rho, n_s, channels.gate_channel_sequence(first, nm_s))
+    times = {k: [] for k in full_cls}
     t0 = time.perf_counter()
-    done = 0
-    for op in c.ops:
-        dense.apply_channel_seq(rho, n_s, channels.gate_channel_sequence(op, nm))
-        done += 1
-        if time.perf_counter() - t0 > budget_s and done >= 2:
+    while True:
+        for k in full_cls:
+            inst = samp_cls[k]           # instances spread over the circuit (golden-ratio stride)
+            op = inst[int(len(times[k]) * 0.6180339887 * len(inst) + len(inst) // 2) % len(inst)]
+            a = time.perf_counter()
+            dense.apply_channel_seq(rho, n_s, channels.gate_channel_sequence(op, nm_s))
+            times[k].append(time.perf_counter() - a)
+        if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    per_gate = dt / done * 4 ** (n_full - n_s)          # O(4^n) per gate
-    t_circuit = per_gate * len(c_full.ops)
-    value = ops_fused / t_circuit
     del rho
-    sample = (f"oracle (oracle/dense.c, OpenMP) applied the first {done} of {len(c.ops)} "
-              f"basis gates (noise channels unfused) of the same {config=} workload at n={n_s} "
-              f"in {dt:.2f} s; per-gate time scaled by 4^({n_full}-{n_s}) to n={n_full} and "
-              f"multiplied by the {len(c_full.ops)} gates of the full circuit "
-              f"({t_circuit:.1f} s); value = the GPU plan's fused-gate updates per circuit / that time")
-    return {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": sample, "seconds": dt}
+    scale = 4.0 ** (n_full - n_s)
+    per = {k: statistics.fmean(v) for k, v in times.items()}
+    t_circuit = sum(len(full_cls[k]) * per[k] * scale for k in full_cls)
+    desc = "; ".join(f"{k[0]}(k={k[1]}, {len(k[2])} channels) x{len(full_cls[k])}: "
+                     f"{per[k] * 1e3:.0f} ms at n={n_s} ({len(times[k])} runs)" for k in full_cls)
+    sample = (f"oracle (oracle/dense.c, OpenMP, all host cores) timed one instance of each of the "
+              f"{len(full_cls)} channel-sequence classes of the config-{config} circuit on a dense "
+              f"n={n_s} rho for {dt:.1f} s [{desc}]; circuit time = sum over the {len(c_full.ops)} "
+              f"basis gates of the n={n_full} circuit of their class time x 4^({n_full}-{n_s}) = "
+              f"{t_circuit:.0f} s; value = the GPU plan's {gate_updates} fused-gate updates per "
+              f"circuit / that time")
+    return {"value": gate_updates / t_circuit, "unit": UNIT, "cores": os.cpu_count(),
+            "kind": "oracle", "sample": sample, "seconds": dt, "circuit_s_estimated": t_circuit}
+
+
+def oracle_whole_circuit(config: int, n: int):
+    """The whole config circuit at a small n, oracle end to end (no sampling, no scaling)."""
+    import workloads as W
+    from oracle import dense
+    c, nm = W.config_workload(config, n=n)
+    dense.lib()
+    t0 = time.perf_counter()
+    rho = dense.run(c, nm)
+    p = dense.probs(rho, n, dense.readout_of(nm))
+    dt = time.perf_counter() - t0
+    return dt, p, c, nm
+
+
+def workload_config(args, c, counts) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
+            "n_qubits": c.n, "gates": len(c.ops), "gate_updates": counts["gate_updates"],
+            "fusion": f"fuse={args.fuse} k_max={args.kmax}", "state_bytes": 16 * 4 ** c.n,
+            "l2": ("inputs larger than L2 (state >> 126 MB)" if 16 * 4 ** c.n > 5e8
+                   else "state fits L2 (no flush)")}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
     import workloads as W
     c, nm = W.config_workload(args.config, n=args.n)
-    # the fused op count the GPU arm executes per circuit (host planner, no GPU needed)
-    ops_fused = fused_count_host(c, nm, args)
+    counts = plan_counts(args.config, c.n, world, args.fuse, args.kmax)
+    for _ in range(args.warmup):
+        oracle_estimate(args.config, c.n, counts["gate_updates"], budget_s=args.ref_budget / 4)
     vals = []
     t0 = time.perf_counter()
     cb = None
     for _ in range(args.steps):
-        cb = oracle_sample(args.config, c.n, ops_fused, budget_s=args.ref_budget)
+        cb = oracle_estimate(args.config, c.n, counts["gate_updates"], budget_s=args.ref_budget)
         vals.append(cb["value"])
     wall = time.perf_counter() - t0
     value = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
-                       "n_qubits": c.n, "gates": len(c.ops), "gate_updates": ops_fused},
+            "config": workload_config(args, c, counts),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"],
                              "kind": "oracle", "sample": cb["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -174,11 +241,37 @@ def run_reference(args):
     return 0
 
 
-def fused_count_host(c, nm, args) -> int:
-    """Fused op count of the GPU arm's plan (host planner only, no device work)."""
-    from paper_2404_13184_b200.tanq import Plan
-    p = Plan(None, c, nm, fuse=args.fuse, k_max=args.kmax, world_size=args.gpus)
-    return p.info()["gate_updates"]
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def build_nccl_shim() -> str:
+    """tests/nccl_shim: host-staged stand-in for the NCCL calls libtanq makes, for running N
+    ranks on fewer GPUs (a functional check of the N > 1 path, never a multi-GPU timing)."""
+    out = os.path.join("/tmp", f"tanq_nccl_shim_{os.getuid()}.so")
+    src = os.path.join(ROOT, "tests", "nccl_shim", "nccl_shim.cpp")
+    subprocess.check_call(["g++", "-O2", "-shared", "-fPIC", "-std=c++17",
+                           "-I/usr/local/cuda/include", src, "-o", out,
+                           "-L/usr/local/cuda/lib64", "-lcudart", "-lpthread"])
+    return out
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without torchrun: start the N ranks here (one process per GPU,
+    torch.distributed.run on 127.0.0.1).  With fewer GPUs than N the ranks share them through
+    the NCCL test shim and the line says so (functional check, not a timing)."""
+    import torch
+    env = dict(os.environ)
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if ndev < args.gpus and not env.get("TANQ_NCCL_LIB"):
+        env["TANQ_NCCL_LIB"] = build_nccl_shim()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # --------------------------------------------------------------------------------------
@@ -230,7 +323,14 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
     sim.set_stream(stream.cuda_stream)
     ro = CReadout.of(nm)
+    t_plan = time.perf_counter()
     plan = Plan(sim, c, nm, fuse=args.fuse, k_max=args.kmax, profile=True)
+    plan_wall_ms = (time.perf_counter() - t_plan) * 1e3
+    counts = plan_counts(args.config, n, world, args.fuse, args.kmax)
+    pinfo = plan.info()
+    if pinfo["gate_updates"] != counts["gate_updates"]:
+        raise SystemExit(f"workloads/plan_counts.json is stale ({counts['gate_updates']} vs "
+                         f"{pinfo['gate_updates']} updates): run scripts/plan_counts.py")
 
     def step():
         sim.reset()
@@ -288,6 +388,16 @@ def run_ours(args):
     hw_tf = hw_flops_launch / (avg_ms * 1e-3) / 1e12
     t_hbm = bytes_launch / (peak_gbs * 1e9)
     t_fp = flops_launch / (peak_tf * 1e12)
+    # the same launch in SURVEY §8(d)'s full-state basis: 32 B and 8 * 4^k flops per amplitude
+    # of all 4^n / G amplitudes (the packed layout touches 16 B and does half of those flops)
+    packed = gate["bytes"] > 0 and abs(bytes_launch / (16.0 * 2 ** info["local_bits"]) - 1) < 1e-9
+    full_f = 2.0 if packed else 1.0
+    full_basis = {
+        "basis": "SURVEY §8(d) full state: 32 B and 8*4^k flops per amplitude of all 4^n/G "
+                 "amplitudes per pass" + (" (2x the packed launch's own counts)" if packed else ""),
+        "bytes_per_launch": bytes_launch * full_f, "flops_per_launch": flops_launch * full_f,
+        "hbm_gbs_equiv": gbs * full_f, "hbm_frac_equiv": gbs * full_f / peak_gbs,
+        "fp64_tflops_equiv": tf * full_f, "fp64_frac_equiv": tf * full_f / peak_tf}
     common = {"kernel": gate["name"], "traffic": traffic, "traffic_source": traffic_src,
               "algorithmic_bytes_per_launch": bytes_launch, "flops_per_launch": flops_launch,
               "avg_launch_ms": avg_ms, "launches": gate["launches"], "share_of_step": share,
@@ -296,9 +406,12 @@ def run_ours(args):
               "fp64_hw_frac": hw_tf / peak_tf, "fp64_peak": peak_tf,
               "fp64_peak_kind": peak_tf_kind,
               "floors_ms": {"hbm": t_hbm * 1e3, "fp64": t_fp * 1e3},
+              "basis": ("packed Hermitian layout: 16 B per amplitude per pass and half the "
+                        "flops (only the canonical element of each transpose pair is "
+                        "processed)" if packed else "full layout: 32 B per amplitude per pass"),
+              "full_state_basis": full_basis,
               "flops_note": "algorithmic flops = 8 per complex multiply-add; the DMMA kernels "
-                            "execute 6 (3-multiply complex product); packed-layout launches "
-                            "count 16 B and half the flops per amplitude"}
+                            "execute 6 (3-multiply complex product)"}
     if t_fp > t_hbm:
         roofline = {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": tf / peak_tf, "peak_kind": peak_tf_kind, **common}
@@ -308,7 +421,7 @@ def run_ours(args):
                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", **common}
 
     # ---- e2e: the public API from host objects, H2D of the inputs, D2H of the result ----
-    t_e2e = []
+    t_e2e, plan_ms_e2e = [], []
     for _ in range(max(1, args.steps)):
         torch.cuda.synchronize()
         a0 = time.perf_counter()
@@ -317,6 +430,7 @@ def run_ours(args):
         p = sim.probs(CReadout.of(nm))
         torch.cuda.synchronize()
         t_e2e.append(time.perf_counter() - a0)
+        plan_ms_e2e.append(st2["plan_ms"])
     e2e_s = statistics.median(t_e2e)
     if world > 1:
         t = torch.tensor([e2e_s], device=tdev, dtype=torch.float64)
@@ -327,8 +441,36 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(args.config, n, ops, budget_s=args.ref_budget)
+        cpu = oracle_estimate(args.config, n, ops, budget_s=args.ref_budget)
         cpu.pop("seconds", None)
+        if args.whole_n:
+            # the whole circuit at a small n, oracle end to end beside the GPU on the same plan
+            wt, wp, wc, wnm = oracle_whole_circuit(args.config, args.whole_n)
+            with Simulator(args.whole_n) as ws:
+                ws.set_stream(stream.cuda_stream)
+                wplan = Plan(ws, wc, wnm, fuse=args.fuse, k_max=args.kmax)
+                for _ in range(3):
+                    ws.reset()
+                    wplan.exec(ws)
+                reps = 20
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(stream)
+                for _ in range(reps):
+                    ws.reset()
+                    wst = wplan.exec(ws)
+                    gp = ws.probs(CReadout.of(wnm))
+                f1.record(stream)
+                torch.cuda.synchronize()
+                g_s = f0.elapsed_time(f1) / 1e3 / reps
+            cpu["whole_circuit"] = {
+                "n_qubits": args.whole_n, "basis_gates": len(wc.ops),
+                "gate_updates": wst["gate_updates"], "oracle_s": wt, "gpu_s": g_s,
+                "oracle_updates_per_s": wst["gate_updates"] / wt,
+                "gpu_updates_per_s": wst["gate_updates"] / g_s,
+                "max_abs_probs_diff": float(np.abs(gp - wp).max()),
+                "note": "whole circuit, no sampling or scaling: the oracle end to end on all "
+                        "host cores vs the GPU plan on the same circuit (readout-noisy probs "
+                        "compared); at this n the GPU is launch-bound, so the ratio is a floor"}
 
     if rank == 0:
         line = {
@@ -336,20 +478,17 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES.get(args.config, str(args.config)),
-                       "n_qubits": n, "gates": len(c.ops), "gate_updates": ops,
-                       "kernel_ops": st["ops_fused"],
-                       "fusion": f"fuse={args.fuse} k_max={args.kmax}",
-                       "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
-                       "remaps_per_step": st["n_remaps"],
-                       "state_bytes": 16 * 4 ** n, "shard_bytes": info["shard_bytes"],
-                       "parallelism": (f"{world} ranks sharing GPU(s) through the NCCL test shim "
-                                       f"(functional check, not a timing)" if shim and world > 1 else
-                                       f"state partitioned over {world} GPU(s) by high bits"
-                                       if args.shards == 1 else
-                                       f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
-                       "l2": "inputs larger than L2 (state >> 126 MB)" if 16 * 4 ** n > 5e8
-                       else "state fits L2 (no flush)"},
+            "config": workload_config(args, c, counts),
+            "parallelism": (f"{world} ranks sharing GPU(s) through the NCCL test shim "
+                            f"(functional check, not a timing)" if shim and world > 1 else
+                            f"state partitioned over {world} GPU(s) by high bits"
+                            if args.shards == 1 else
+                            f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
+            "plan": {"kernel_ops": st["ops_fused"],
+                     "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
+                     "remaps_per_step": st["n_remaps"], "shard_bytes": info["shard_bytes"],
+                     "plan_ms": pinfo["plan_ms"], "plan_wall_ms": plan_wall_ms,
+                     "e2e_plan_ms": statistics.median(plan_ms_e2e)},
             "hbm_gbs": hbm_total / (ms / 1e3) / 1e9,
             "amplitude_updates_per_s": value * 4 ** n,
             "circuit_gates_per_s": len(c.ops) * args.steps / (ms / 1e3),
@@ -384,7 +523,11 @@ def main():
                     help="qubits of the workload (--qubits under torchrun: it claims --n)")
     ap.add_argument("--fuse", type=int, default=2)
     ap.add_argument("--kmax", type=int, default=3)
-    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=8.0,
+                    help="seconds of oracle work per cpu_baseline / reference step")
+    ap.add_argument("--whole-n", type=int, default=None,
+                    help="N=1: also run the whole config circuit at this n on the oracle beside "
+                         "the GPU (default: 12 for config 4, else skipped; 0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shards", type=int, default=1,
                     help="N=1 only: split the state into this many virtual shards on the one GPU "
@@ -392,8 +535,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.whole_n is None:
+        args.whole_n = 12 if args.config == 4 else 0
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_ours(args)
 
 

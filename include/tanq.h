@@ -263,10 +263,11 @@ tanq_status tanq_set_state(tanq_sim* s, uint64_t first, uint64_t count, const ta
 tanq_status tanq_sync(tanq_sim* s);
 const char* tanq_last_error(void);
 
-/* Mirror mode: while rho is known to be Hermitian and an op is
+/* Packed Hermitian layout: while rho is known to be Hermitian and an op is
  * Hermiticity-preserving (every Kraus-form op; user superoperators are checked), single-shard
- * handles read and compute only one tuple of each transpose pair and write the other as its
- * conjugate (24 instead of 32 B per amplitude, half the FP64 work).  rho is known Hermitian
+ * handles keep only the canonical element of each transpose pair up to date and every kernel
+ * reads and writes only those (16 instead of 32 B per amplitude per pass, half the FP64 work);
+ * the other half is restored by one unpack pass before anything reads it.  rho is known Hermitian
  * after create / reset; tanq_set_state clears it; this call measures max|rho - rho^dag| and
  * sets it when <= tol * max(1, max|rho|).  Disable with env TANQ_MIRROR=0 or run flag bit2. */
 tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm);

@@ -1087,7 +1087,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   }
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
-    // mirror mode reads only the canonical half of the tuples: 24 B / amplitude, half the flops
+    // packed layout: only the canonical element of each transpose pair is read and written
+    // (16 B per amplitude per pass) and half the tuples are computed
     const bool mir = mir_op;
     const double fr = mir ? 0.5 : 1.0;
     Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 16.0 : 32.0) * amps,

@@ -17,11 +17,44 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "tanq_internal.h"
 
 namespace tanq {
 
 static constexpr int kThreads = 256;
+
+// cudaFuncSetAttribute applies to the current device only: raise the dynamic shared-memory
+// limit once per (kernel, device) -- a handle may spread shards over several devices.
+template <typename Kern>
+static cudaError_t ensure_smem_attr(Kern kern, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = (uint64_t)1 << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done.fetch_or(bit);
+  return e;
+}
+
+// Debug / test knob (env TANQ_GRID_CAP=N, default off): cap the grid of the persistent group,
+// tile and DMMA k=2 kernels at N CTAs so that small registers still run many tiles per warp
+// (the loop paths a full-size launch takes).  Never set in production.
+static unsigned grid_cap() {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("TANQ_GRID_CAP");
+    cap = e ? atoi(e) : 0;
+    if (cap < 0) cap = 0;
+  }
+  return (unsigned)cap;
+}
+static inline unsigned capped(unsigned g) {
+  const unsigned c = grid_cap();
+  return (c && g > c) ? c : g;
+}
 
 static inline unsigned grid_for(uint64_t work, int threads, uint64_t cap = 148ull * 64) {
   uint64_t g = (work + threads - 1) / threads;
@@ -362,7 +395,7 @@ cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st) {
   uint64_t warps = tiles;
   const uint64_t cap = 148ull * 16;  // one wave: 2 CTAs x 8 warps per SM, persistent
   if (warps > cap) warps = cap;
-  unsigned grid = (unsigned)((warps + 7) / 8);
+  unsigned grid = capped((unsigned)((warps + 7) / 8));
   if (p.pos[0] == 0)
     gate2_mma_kernel<false><<<grid, 256, 0, st>>>(a, p);
   else
@@ -746,22 +779,19 @@ static size_t group_smem(const GroupParams& p) {
 
 template <int NQ, int WARPS, int NBUF, bool HAS3, int UI>
 static cudaError_t launch_group_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
-  static bool attr_set = false;
+  static std::atomic<uint64_t> attr_done{0};
   constexpr int T = 1 << (9 - 2 * NQ);
   const size_t smem = group_smem<NQ, WARPS, NBUF, HAS3, UI>(p);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = group_kernel<NQ, WARPS, NBUF, HAS3, UI>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t ea = ensure_smem_attr(kern, attr_done);
+  if (ea != cudaSuccess) return ea;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t tiles = (p.n_tuples + T - 1) / T;
   const uint64_t ctas = (tiles + WARPS - 1) / WARPS;
-  unsigned grid = (unsigned)(ctas < (uint64_t)sms ? ctas : (uint64_t)sms);
+  unsigned grid = capped((unsigned)(ctas < (uint64_t)sms ? ctas : (uint64_t)sms));
   if (grid < 1) grid = 1;
   kern<<<grid, WARPS * 32, smem, st>>>(a, p);
   return cudaGetLastError();
@@ -946,17 +976,14 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
 
 template <int NQ, int WARPS, int NBUF, int UI>
 static cudaError_t launch_tile_cfg(double2* a, const GroupParams& p, cudaStream_t st) {
-  static bool attr_set = false;
+  static std::atomic<uint64_t> attr_done{0};
   constexpr int TT = WARPS << (9 - 2 * NQ);
   const size_t smem = (size_t)((p.prog_elems + 7) & ~7) * sizeof(double2) +
                       (size_t)NBUF * WARPS * 512 * sizeof(double2) + 32 * 8 + 32 * 4 +
                       (size_t)p.n_sub * sizeof(GroupSub);
   auto kern = tile_kernel<NQ, WARPS, NBUF, UI>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t ea = ensure_smem_attr(kern, attr_done);
+  if (ea != cudaSuccess) return ea;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -965,7 +992,7 @@ static cudaError_t launch_tile_cfg(double2* a, const GroupParams& p, cudaStream_
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t tiles = (p.n_tuples + TT - 1) / TT;
   const uint64_t cap = (uint64_t)sms * per_sm;
-  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+  const unsigned grid = capped((unsigned)(tiles < cap ? tiles : cap));
   kern<<<grid, WARPS * 32, smem, st>>>(a, p);
   return cudaGetLastError();
 }

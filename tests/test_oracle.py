@@ -174,6 +174,55 @@ def test_overrotation_x_on_zero():
     assert abs(np.trace(rho @ rho) - 1) < 1e-14
 
 
+def test_overrotation_two_qubit_axis_closed_form():
+    """Reading R10: 2q over-rotation E = exp(-i eps Z_control X_target / 2) after CX.
+    On |c=1,t=0>: CX -> |11>, then E|11> = cos(eps/2)|11> + i sin(eps/2)|c=1,t=0> (Z_c = -1,
+    X_t flips t).  On |00>: E|00> = cos(eps/2)|00> - i sin(eps/2)|c=0,t=1>.  A swapped axis
+    (X_c Z_t) would move the sin^2 weight to the other basis state, so this fixes which factor
+    is Z.  Outcome index bit q = qubit q; control = qubit 0, target = qubit 1."""
+    for eps in (0.3, -0.05, 1.7):
+        c, s = math.cos(eps / 2), math.sin(eps / 2)
+        nm = W.NoiseModel(2, [W.QubitCal(), W.QubitCal()])
+        nm.gates[("x", (0,))] = W.GateCal(0.0, 0.0, 0.0)
+        nm.gates[("cx", (0, 1))] = W.GateCal(0.0, 0.0, eps)
+        rho = dense.run(W.Circuit(2, [W.Op("x", (0,)), W.Op("cx", (0, 1))]), nm)
+        psi = np.zeros(4, dtype=complex)
+        psi[3], psi[1] = c, 1j * s                      # |c=1,t=1>, |c=1,t=0>
+        assert np.abs(rho - np.outer(psi, psi.conj())).max() < 1e-15
+        rho = dense.run(W.Circuit(2, [W.Op("cx", (0, 1))]), nm)
+        psi = np.zeros(4, dtype=complex)
+        psi[0], psi[2] = c, -1j * s                     # |00>, |c=0,t=1>
+        assert np.abs(rho - np.outer(psi, psi.conj())).max() < 1e-15
+
+
+def test_channel_order_closed_form():
+    """Reading R5: order=0 applies thermal relaxation before depolarizing, order=1 after.
+    X on |0> with AD(gamma) (+ PD, diagonal-neutral) and depolarizing p, closed forms:
+      order 0: P(1) = (1-p)(1-gamma) + p/2      order 1: P(1) = (1-gamma)(1-p/2)
+    (the two differ by p*gamma/2, so the order is pinned, not just self-consistent)."""
+    t1, t2, dur_ns, p = 40.0, 55.0, 900.0, 0.2
+    gamma = 1 - math.exp(-dur_ns * 1e-3 / t1)
+    for order, want in ((0, (1 - p) * (1 - gamma) + p / 2), (1, (1 - gamma) * (1 - p / 2))):
+        nm = W.NoiseModel(1, [W.QubitCal(t1, t2)], order=order)
+        nm.gates[("x", (0,))] = W.GateCal(p, dur_ns, 0.0)
+        rho = dense.run(W.Circuit(1, [W.Op("x", (0,))]), nm)
+        assert abs(rho[1, 1].real - want) < 1e-15, (order, rho[1, 1], want)
+        assert abs(rho[0, 1]) < 1e-15
+
+
+def test_cluster_product_structure():
+    """Pins the full-size parity method of tests/test_gpu_headline.py: a circuit that never
+    couples two clusters yields the tensor product of the clusters' states (oracle vs oracle
+    on relabelled sub-circuits, every entry)."""
+    from _product import expected_columns
+    n = 7
+    c, nm, subs = W.cluster_product_workload(n, [(0, 4), (1, 5, 6), (2, 3)], layers=3, seed=31)
+    full = dense.run(c, nm)
+    parts = [(qs, dense.run(sc, snm)) for qs, sc, snm in subs]
+    E = expected_columns(parts, n, np.arange(2 ** n))          # E[c, r] = rho[r][c]
+    assert np.abs(E.T - full).max() < 1e-14
+
+
 def test_rz_noiseless_under_any_device():
     # P:255: RZ carries no noise even when a calibration entry exists
     nm = W.NoiseModel(1, [W.QubitCal(50.0, 60.0, 0.1, 0.1)])

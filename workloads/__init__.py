@@ -323,6 +323,48 @@ def random_circuit(n: int, n_ops: int, seed: int, kmax: int = 2,
     return Circuit(n, ops, name=f"random_n{n}_{n_ops}")
 
 
+def restrict(circ: Circuit, nm: Optional[NoiseModel], qubits: Sequence[int]):
+    """The ops of `circ` acting inside `qubits` relabelled to 0..k-1 (qubits[j] -> j), with the
+    matching slice of the noise model (relabelling only; no arithmetic of the method)."""
+    loc = {q: j for j, q in enumerate(qubits)}
+    ops = [Op(o.kind, tuple(loc[q] for q in o.qubits), o.theta, o.mat, o.kraus)
+           for o in circ.ops if all(q in loc for q in o.qubits)]
+    sub = Circuit(len(qubits), ops, name=f"{circ.name}|{tuple(qubits)}")
+    if nm is None:
+        return sub, None
+    snm = NoiseModel(len(qubits), [nm.qubits[q] for q in qubits], order=nm.order)
+    for (kind, qs), g in nm.gates.items():
+        if all(q in loc for q in qs):
+            snm.gates[(kind, tuple(loc[q] for q in qs))] = g
+    return sub, snm
+
+
+def cluster_product_workload(n: int, clusters: Sequence[Sequence[int]], layers: int, seed: int,
+                             overrot: bool = True):
+    """A noisy IBM-basis circuit whose gates never couple two clusters of qubits (interleaved in
+    program order across clusters), so rho_out is the tensor product of the clusters' states.
+    Returns (circuit, noise model, [(cluster qubits, sub-circuit, sub-noise model)]).  Used to pin
+    the full-size GPU state element by element against per-cluster oracle runs."""
+    rng = np.random.default_rng(seed)
+    qs_all = sorted(q for c in clusters for q in c)
+    assert qs_all == list(range(n)), "clusters must partition the register"
+    ops: List[Op] = []
+    for _ in range(layers):
+        for cl in clusters:
+            for q in cl:
+                a, b = rng.uniform(0, 2 * math.pi, 2)
+                ops += [Op("rz", (q,), a), Op("sx", (q,)), Op("rz", (q,), b)]
+        for cl in clusters:
+            perm = [int(x) for x in rng.permutation(list(cl))]
+            for i in range(0, len(perm) - 1, 2):
+                ops.append(Op("cx", (perm[i], perm[i + 1])))
+            if len(perm) >= 3:
+                ops.append(Op("cx", (perm[1], perm[2])))
+    circ = Circuit(n, ops, name=f"clusters_n{n}_l{layers}")
+    nm = synthetic_calibration(circ, seed, depol=True, thermal=True, overrot=overrot)
+    return circ, nm, [(tuple(cl),) + restrict(circ, nm, cl) for cl in clusters]
+
+
 CONFIGS = {
     1: "3-qubit GHZ + depolarizing gate noise + readout (paper worked example)",
     2: "10-qubit QFT, thermal relaxation + coherent over-rotation",

@@ -233,6 +233,15 @@ tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* item
  * in the paper's vec convention (local index r + c 2^k over qubits[0..k-1]).  For a K3 group
  * this is the product of its sub-ops. */
 tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits, tanq_c64* S);
+/* Instrumentation (tests): the block-pipeline kernel program of plan op i on a
+ * single-shard register in the initial layout, packed = 1 for the packed Hermitian layout.
+ * params receives the kernel's parameter struct (params_size must equal its size), blob the
+ * fragments + shared-memory offset tables (*blob_bytes).  *kind = 2 if the block kernel would
+ * run the op, else 0 (nothing written).  Host only; no device work. */
+tanq_status tanq_plan_block_program(const tanq_plan* p, uint64_t i, int packed, void* params,
+                                    size_t params_size, void* blob, size_t blob_cap, int* kind,
+                                    size_t* blob_bytes);
+
 
 /* ---- reductions from the diagonal ---------------------------------------------------- */
 

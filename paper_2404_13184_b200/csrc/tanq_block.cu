@@ -1,0 +1,395 @@
+// K3 "block pipeline" kernel (round 2): a fused group of k <= 2 sub-ops on 2 or
+// 3 qubits applied to the state in one HBM round trip, with the HBM traffic moved by the
+// asynchronous bulk-copy engine so that it overlaps the FP64 tensor work.
+//
+// Data unit: a block = 5 whole qubits -- the group's qubits plus the lowest free qubits --
+// i.e. 10 physical index bits, 1024 amplitudes, 16 KB.  Its lowest 4 bits are always physical
+// bits 0..3 (qubits 0 and 1 are in every block), so a block is 64 contiguous 256 B pieces.
+// Each pair of warps owns two block stages in shared memory:
+//
+//   load     every pair thread issues one cp.async.bulk (global -> shared) of its piece,
+//            signalling the stage's mbarrier (arrive.expect_tx 256 B each, 64 arrivals);
+//   wait     both warps wait on the mbarrier (phase parity);
+//   fixup    packed layout only: pieces read from the transposed position are permuted
+//            (swap of each qubit's row/col bit inside the piece) and conjugated in place;
+//            self-transposed blocks are symmetrised (non-canonical <- conj(canonical));
+//   compute  each warp applies the group's sub-ops to its half of the block (8 tuples x 64
+//            members for 3-qubit groups): k=2 sub-ops on the FP64 tensor pipe
+//            (mma.sync.m8n8k4.f64 -> DMMA.8x8x4), k=1 sub-ops as DFMA streams;
+//   store    unfixup, fence.proxy.async, one cp.async.bulk (shared -> global) per piece back
+//            to where the piece came from; the stage is refilled with the pair's next block
+//            after cp.async.bulk.wait_group.read -- one iteration later, so the copy of block
+//            i+1 runs during the compute of block i and the stores drain behind it.
+//
+// Pieces are placed in shared memory at 16 * rank + G(piece) units (16 B), G a per-launch
+// linear bank rotation chosen by the host so that the DMMA B-fragment loads and D-fragment
+// stores of every sub-op are (near) bank-conflict free; every lane's shared-memory offsets
+// come from per-sub-op tables built by the host (tanq_host.cpp: build_block).
+//
+// Complex arithmetic, per k=2 sub-op (S = a + ib, x = c + id), three real products with no
+// epilogue additions:  k1 = a(c+d);  Re y = k1 - (a+b) d;  Im y = k1 + (b-a) c, where the
+// second and third products accumulate onto k1 (DMMA with C = k1).  a, -(a+b) and (b-a) are
+// precomputed fragments, so the only FP64 adds left are the c+d of each B element.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <atomic>
+
+#include "tanq_internal.h"
+
+namespace tanq {
+
+namespace {
+
+__device__ __forceinline__ uint64_t pair_swap64(uint64_t x) {
+  return ((x & 0x5555555555555555ull) << 1) | ((x >> 1) & 0x5555555555555555ull);
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void pair_bar(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+// D = A B + C with C and D distinct
+__device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b, double c0,
+                                       double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+__device__ __forceinline__ uint64_t insert_zeros10(uint64_t t, const uint64_t* lo) {
+#pragma unroll
+  for (int j = 0; j < 10; ++j) t = ((t & ~lo[j]) << 1) | (t & lo[j]);
+  return t;
+}
+
+// 16-element piece, in-piece index t = (r0 c0 r1 c1): transpose swaps each row/col bit pair.
+__device__ __forceinline__ int pswap4(int t) { return ((t & 5) << 1) | ((t >> 1) & 5); }
+
+// In-place (permute + conjugate) of one piece: X[pswap4(t)] <- conj(X[t]).  Involution.  The
+// start offset `rot` spreads the lanes of a warp over the banks.
+__device__ __forceinline__ void piece_transpose(double2* P, int rot) {
+  double2 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = P[(i + rot) & 15];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) P[pswap4((i + rot) & 15)] = make_double2(v[i].x, -v[i].y);
+}
+
+// k = 2 sub-op on one warp's half block.  F: fragments [3][2 mt][4 ks][32 lanes] doubles
+// (a, -(a+b), b-a); T: this lane's 32 offsets (16 B-fragment [ks][j], 16 D-fragment [mt][j][c]).
+template <int UI>
+__device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const uint16_t* T,
+                                           int lane) {
+  double a1[2][4], a2[2][4], a3[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      a1[mt][ks] = F[(0 * 8 + mt * 4 + ks) * 32 + lane];
+      a2[mt][ks] = F[(1 * 8 + mt * 4 + ks) * 32 + lane];
+      a3[mt][ks] = F[(2 * 8 + mt * 4 + ks) * 32 + lane];
+    }
+  uint32_t ob[8], od[8];  // packed uint16 pairs
+  {
+    const uint4* t4 = reinterpret_cast<const uint4*>(T);
+    const uint4 b0 = t4[0], b1 = t4[1], d0 = t4[2], d1 = t4[3];
+    ob[0] = b0.x; ob[1] = b0.y; ob[2] = b0.z; ob[3] = b0.w;
+    ob[4] = b1.x; ob[5] = b1.y; ob[6] = b1.z; ob[7] = b1.w;
+    od[0] = d0.x; od[1] = d0.y; od[2] = d0.z; od[3] = d0.w;
+    od[4] = d1.x; od[5] = d1.y; od[6] = d1.z; od[7] = d1.w;
+  }
+  auto boff = [&](int ks, int j) {
+    const int e = ks * 4 + j;
+    return (int)((ob[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+  };
+  auto doff = [&](int mt, int j, int c) {
+    const int e = (mt * 4 + j) * 2 + c;
+    return (int)((od[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+  };
+#pragma unroll
+  for (int n0 = 0; n0 < 4; n0 += UI) {
+    double2 xb[UI][4];
+#pragma unroll
+    for (int u = 0; u < UI; ++u)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) xb[u][ks] = X[boff(ks, n0 + u)];
+    double k1[UI][2][2];
+#pragma unroll
+    for (int u = 0; u < UI; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) k1[u][mt][0] = k1[u][mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+      for (int u = 0; u < UI; ++u) {
+        const double s = xb[u][ks].x + xb[u][ks].y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], s);
+      }
+    double yr[UI][2][2], yi[UI][2][2];
+#pragma unroll
+    for (int u = 0; u < UI; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb[u][0].y, k1[u][mt][0], k1[u][mt][1]);
+        dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb[u][0].x, k1[u][mt][0], k1[u][mt][1]);
+      }
+#pragma unroll
+    for (int ks = 1; ks < 4; ++ks)
+#pragma unroll
+      for (int u = 0; u < UI; ++u)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
+          dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+        }
+    __syncwarp();  // every lane's B loads of this pass precede any lane's D stores
+#pragma unroll
+    for (int u = 0; u < UI; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          X[doff(mt, n0 + u, c)] = make_double2(yr[u][mt][c], yi[u][mt][c]);
+  }
+}
+
+// k = 1 sub-op (4x4 complex, DFMA): T = this lane's 16 offsets [j column][i member].
+__device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const uint16_t* T) {
+  const double2* S = reinterpret_cast<const double2*>(F);
+  uint32_t o[8];
+  {
+    const uint4* t4 = reinterpret_cast<const uint4*>(T);
+    const uint4 a = t4[0], b = t4[1];
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+    o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  }
+  auto off = [&](int j, int i) {
+    const int e = j * 4 + i;
+    return (int)((o[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+  };
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double2 x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = X[off(j, i)];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      double yr = 0.0, yi = 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double2 s = S[l * 4 + m];
+        yr = fma(s.x, x[m].x, yr);
+        yr = fma(-s.y, x[m].y, yr);
+        yi = fma(s.x, x[m].y, yi);
+        yi = fma(s.y, x[m].x, yi);
+      }
+      X[off(j, l)] = make_double2(yr, yi);
+    }
+  }
+}
+
+}  // namespace
+
+constexpr int kStageUnits = 1032;  // 16 x 64 + rotation slack (<= 7), rounded to 8 units
+
+template <int UI>
+__global__ void __launch_bounds__(384, 1)
+    block_kernel(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);  // [2 * kMaxPairs]
+  unsigned char* sBlob = smem_raw + 16 * kBlockMaxPairs;
+  double2* sStage = reinterpret_cast<double2*>(sBlob + p.blob_bytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, half = warp & 1, pt = threadIdx.x & 63;
+
+  {  // blob (sub-op fragments + offset tables) -> shared; mbarrier init
+    const uint4* src = reinterpret_cast<const uint4*>(p.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sBlob);
+    for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x < 2 * p.pairs) mbar_init(&mbar[threadIdx.x], 64);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (pair >= p.pairs) return;
+
+  double2* stage0 = sStage + (size_t)pair * 2 * kStageUnits;
+  const uint64_t goff = p.piece_goff[pt];
+  const int sstart = p.piece_start[pt];
+  const int rot = pt & 15;
+  const uint64_t nb = p.n_blocks;
+  const uint64_t npairs = (uint64_t)gridDim.x * p.pairs;
+  const bool mirror = p.mirror != 0;
+  auto next_block = [&](uint64_t i) {
+    if (mirror)
+      while (i < nb && i > pair_swap64(i)) i += npairs;
+    return i;
+  };
+  // where this thread's piece of block i lives: in place, or (packed layout, non-canonical
+  // piece of a block that is not self-transposed) at the transposed position
+  auto piece_src = [&](uint64_t i, bool& tr) {
+    const uint64_t base = insert_zeros10(i, p.lo_mask);
+    const uint64_t e0 = base + goff;
+    const uint64_t em = pair_swap64(e0);
+    tr = mirror && pair_swap64(base) != base && e0 > em;
+    return tr ? em : e0;
+  };
+  auto issue = [&](uint64_t i, int s, bool& tr) {
+    const uint64_t src = piece_src(i, tr);
+    uint64_t* bar = &mbar[pair * 2 + s];
+    if (p.dbg & 2) {
+      mbar_arrive_tx(bar, 0);
+    } else {
+      mbar_arrive_tx(bar, 256);
+      bulk_g2s(stage0 + s * kStageUnits + sstart, a + src, 256, bar);
+    }
+  };
+
+  // this pair's blocks b0, b1, ...: b_k is computed in iteration k from stage k % 2; stages
+  // start with b0 and b1; from iteration 1 on, iteration k refills the stage stored in
+  // iteration k-1 with b_{k+1} (after the copy engine has read the stored pieces out)
+  uint64_t cur = next_block((uint64_t)blockIdx.x * p.pairs + pair);
+  uint64_t nxt = cur < nb ? next_block(cur + npairs) : nb;
+  bool tr[2] = {false, false};
+  if (cur < nb) issue(cur, 0, tr[0]);
+  if (nxt < nb) issue(nxt, 1, tr[1]);
+  uint32_t parity[2] = {0u, 0u};
+  bool first = true;
+  int s = 0;
+  while (cur < nb) {
+    double2* X = stage0 + s * kStageUnits;
+    mbar_wait(&mbar[pair * 2 + s], parity[s]);
+    parity[s] ^= 1u;
+    const uint64_t base = insert_zeros10(cur, p.lo_mask);
+    const bool self = mirror && pair_swap64(base) == base;
+    if (tr[s]) piece_transpose(X + sstart, rot);
+    if (self) {  // non-canonical element <- conj(its transpose, canonical, same block)
+      for (int k = 0; k < 16; ++k) {
+        const int idx = pt * 16 + ((k + pt) & 15);
+        const int idm = ((idx & 0x155) << 1) | ((idx >> 1) & 0x155);
+        if (idx > idm) {
+          const double2 v = X[p.start_by_pidx[idm >> 4] + (idm & 15)];
+          X[p.start_by_pidx[idx >> 4] + (idx & 15)] = make_double2(v.x, -v.y);
+        }
+      }
+    }
+    pair_bar(pair);
+    if (!first) {  // refill the other stage (stored last iteration) with the next block
+      bulk_wait_read0();
+      if (nxt < nb) issue(nxt, s ^ 1, tr[s ^ 1]);
+    }
+    if (!(p.dbg & 1)) {
+      for (int q = 0; q < p.n_sub; ++q) {
+        const BlockSub& g = p.sub[q];
+        const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off +
+                            (half * 32 + lane) * (g.k == 2 ? 32 : 16);
+        if (g.k == 2)
+          blk_sub_k2<UI>(X, F, T, lane);
+        else
+          blk_sub_k1(X, F, T);
+        __syncwarp();
+      }
+    }
+    pair_bar(pair);
+    if (tr[s]) piece_transpose(X + sstart, rot);
+    fence_async_smem();
+    pair_bar(pair);
+    if (!(p.dbg & 2)) {
+      bool t2;
+      const uint64_t dst = piece_src(cur, t2);
+      bulk_s2g(a + dst, X + sstart, 256);
+      bulk_commit();
+    }
+    first = false;
+    cur = nxt;
+    nxt = cur < nb ? next_block(cur + npairs) : nb;
+    s ^= 1;
+  }
+  bulk_wait0();
+}
+
+template <int UI>
+static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t smem,
+                                    cudaStream_t st) {
+  static std::atomic<uint64_t> attr_done{0};
+  auto kern = block_kernel<UI>;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = (uint64_t)1 << (dev & 63);
+  if (!(attr_done.load() & bit)) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done.fetch_or(bit);
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t want = (p.n_blocks + p.pairs - 1) / p.pairs;
+  unsigned grid = (unsigned)(want < (uint64_t)sms ? want : (uint64_t)sms);
+  const char* cap = getenv("TANQ_GRID_CAP");
+  if (cap && atoi(cap) > 0 && grid > (unsigned)atoi(cap)) grid = (unsigned)atoi(cap);
+  if (grid < 1) grid = 1;
+  kern<<<grid, 64 * p.pairs, smem, st>>>(a, p);
+  return cudaGetLastError();
+}
+
+size_t block_smem_bytes(int pairs, int blob_bytes) {
+  return 16 * kBlockMaxPairs + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
+}
+
+cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st) {
+  const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
+  if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
+  return launch_block_cfg<2>(a, p, smem, st);
+}
+
+}  // namespace tanq

@@ -534,6 +534,14 @@ struct DevScratch {
   size_t frag_elems = 0;
 };
 
+struct tanq_plan;
+struct PlanCacheEntry {
+  std::string key;       // exact serialisation of circuit + noise model + options
+  tanq_plan* plan = nullptr;
+  uint64_t hits = 0;
+  uint64_t last_use = 0;
+};
+
 struct tanq_sim {
   int n = 0, L = 0, world = 1, rank0 = 0;
   bool dist = false;
@@ -565,6 +573,8 @@ struct tanq_sim {
   size_t frag_host_elems = 0;
   cudaEvent_t frag_done = nullptr;
   bool frag_done_pending = false;
+  std::vector<PlanCacheEntry> plan_cache;  // tanq_run_circuit: recently run circuits
+  uint64_t plan_cache_clock = 0;
   cudaStream_t own_streams_of(int dev) const {
     for (auto& p : owned)
       if (p.first == dev) return p.second;
@@ -1045,6 +1055,308 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
   p.prog_elems = (int)off;
 }
 
+// ------------------------------------------------------------------------------------
+// Block-pipeline group programs (tanq_block.cu)
+// ------------------------------------------------------------------------------------
+// A block = the op's 2 NQ physical target bits + the lowest free physical bits, 10 in all
+// (in the packed layout: 5 whole qubits).  Block-order bit j <-> physical position bpos[j]
+// (ascending); bits 0..3 are always physical 0..3 (the free bits fill from 0), so a block is 64
+// contiguous 16-amplitude pieces.  Shared-memory bank of block element idx (16 B units, 8 banks
+// of 16 B): (idx & 7) + G(idx >> 4) mod 8, where the piece placement G is linear in the 6
+// piece-index bits with weights w[4..9] chosen here; w[0..2] = 1, 2, 4 and w[3] = 0 follow from
+// the contiguous 256 B piece.  For each sub-op the lane -> (member, column) assignment of the
+// DMMA fragments is chosen so that the 8 lanes of every quarter-warp hit distinct banks:
+//   B fragment (k-step loads): lanes vary the 2 in-index bits k0, k1 and column bit n0;
+//   D fragment (stores):      lanes vary out-index bit o0 and column bits n1, n2.
+bool block_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TANQ_BLOCK");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+size_t block_sub_bytes(int k) { return k == 2 ? 768 * 8 + 2 * 32 * 32 * 2 : 32 * 8 + 2 * 32 * 16 * 2; }
+
+size_t block_blob_bytes(const FusedOp& op) {
+  size_t b = 0;
+  if (op.sub.empty()) return block_sub_bytes(op.k);
+  for (const auto& sb : op.sub) b += block_sub_bytes(sb.k);
+  return b;
+}
+
+int block_pairs_for(size_t blob_bytes) {
+  for (int P = tanq::kBlockMaxPairs; P >= 3; --P)
+    if (tanq::block_smem_bytes(P, (int)blob_bytes) <= 227 * 1024) return P;
+  return 0;
+}
+
+// Ops the block kernel runs: 3-qubit groups of k <= 2 sub-ops (not dense k = 3 ops), at least
+// 4 blocks, small enough programs.  Env TANQ_BLOCK=0 restores the round-1 group kernels.
+bool block_ok(const tanq_sim* s, const FusedOp& op) {
+  if (!block_enabled() || op.k != 3 || op.sub.empty()) return false;
+  if ((int)op.sub.size() > tanq::kBlockMaxSub || s->L < 12) return false;
+  for (const auto& sb : op.sub)
+    if (sb.k > 2) return false;
+  return block_pairs_for(block_blob_bytes(op)) > 0;
+}
+
+size_t prog_capacity(const FusedOp& op) {
+  return std::max(group_prog_elems(op), (block_blob_bytes(op) + 15) / 16);
+}
+
+int phase_degree(int w0, int w1, int w2) {  // max lanes per bank over the 8 combinations
+  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+  for (int c = 0; c < 8; ++c) {
+    const int b = ((c & 1 ? w0 : 0) + (c & 2 ? w1 : 0) + (c & 4 ? w2 : 0)) & 7;
+    mx = std::max(mx, ++cnt[b]);
+  }
+  return mx;
+}
+
+struct BlockSubChoice {
+  int k0 = 0, k1 = 0, o0 = 0, n[3] = {0, 0, 0}, cost = 0;
+};
+
+// best lane mapping of one sub-op (member / column block bits) for bank weights w
+BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector<int>& col,
+                           const int* w) {
+  BlockSubChoice best;
+  best.cost = 1 << 20;
+  if (k == 1) {  // lanes vary column bits n0..n2 (col = lane + 32 j)
+    for (size_t a = 0; a < col.size(); ++a)
+      for (size_t b = 0; b < col.size(); ++b)
+        for (size_t c = 0; c < col.size(); ++c) {
+          if (a == b || a == c || b == c) continue;
+          const int d = phase_degree(w[col[a]], w[col[b]], w[col[c]]);
+          if (d < best.cost) {
+            best.cost = d;
+            best.n[0] = col[a];
+            best.n[1] = col[b];
+            best.n[2] = col[c];
+          }
+        }
+    return best;
+  }
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j)
+      for (size_t a = 0; a < col.size(); ++a) {
+        const int db = phase_degree(w[mem[i]], w[mem[j]], w[col[a]]);
+        for (int o = 0; o < 4; ++o)
+          for (size_t b = 0; b < col.size(); ++b)
+            for (size_t c = b + 1; c < col.size(); ++c) {
+              if (b == a || c == a) continue;
+              const int dd = phase_degree(w[mem[o]], w[col[b]], w[col[c]]);
+              if (db + dd < best.cost) {
+                best.cost = db + dd;
+                best.k0 = mem[i];
+                best.k1 = mem[j];
+                best.o0 = mem[o];
+                best.n[0] = col[a];
+                best.n[1] = col[b];
+                best.n[2] = col[c];
+              }
+            }
+      }
+  return best;
+}
+
+// Build the block-kernel parameters and blob (fragments + offset tables) of a 3-qubit group for
+// the current layout.  Returns the blob size in bytes (written to `blob`).
+size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, unsigned char* blob) {
+  const int NQ = op.k, MB = 2 * NQ;
+  const MemberMap tile = member_map(s, NQ, op.q);  // group member bit u <-> tile.bits[u].first
+  std::vector<int> tpos(MB);
+  for (int u = 0; u < MB; ++u) tpos[u] = tile.bits[u].first;
+  // block positions: targets + lowest free positions
+  std::vector<int> bpos(tpos);
+  for (int f = 0; (int)bpos.size() < 10; ++f)
+    if (std::find(tpos.begin(), tpos.end(), f) == tpos.end()) bpos.push_back(f);
+  std::sort(bpos.begin(), bpos.end());
+  auto bit_of_pos = [&](int pos) {
+    return (int)(std::find(bpos.begin(), bpos.end(), pos) - bpos.begin());
+  };
+  std::vector<int> is_member(10, -1);  // block bit -> group member bit u, or -1 (tuple bit)
+  for (int u = 0; u < MB; ++u) is_member[bit_of_pos(tpos[u])] = u;
+  int half = -1;                        // warp-half bit: the highest tuple bit
+  for (int j = 9; j >= 0 && half < 0; --j)
+    if (is_member[j] < 0) half = j;
+  std::vector<const FusedOp*> subs;
+  for (const auto& sb : op.sub) subs.push_back(&sb);
+  // member / column block bits of every sub-op
+  std::vector<std::vector<int>> smem_bits(subs.size()), scol_bits(subs.size());
+  std::vector<MemberMap> smap(subs.size());
+  for (size_t i = 0; i < subs.size(); ++i) {
+    smap[i] = member_map(s, subs[i]->k, subs[i]->q);
+    for (int t = 0; t < 2 * subs[i]->k; ++t) smem_bits[i].push_back(bit_of_pos(smap[i].bits[t].first));
+    for (int j = 0; j < 10; ++j)
+      if (j != half && std::find(smem_bits[i].begin(), smem_bits[i].end(), j) == smem_bits[i].end())
+        scol_bits[i].push_back(j);
+  }
+  // piece-placement weights: start from one rotation per qubit pair of piece-index bits,
+  // (1,2), (4,1), (2,4) (conflict-free for every pair of 3 group qubits when the group sits
+  // above qubit 1), then coordinate descent
+  int w[10] = {1, 2, 4, 0, 0, 0, 0, 0, 0, 0};
+  {
+    static const int init[3][2] = {{1, 2}, {4, 1}, {2, 4}};
+    int qi = 0;
+    for (int j = 4; j + 1 < 10; j += 2)
+      if (is_member[j] >= 0 && is_member[j + 1] >= 0 && qi < 3) {
+        w[j] = init[qi][0];
+        w[j + 1] = init[qi][1];
+        ++qi;
+      }
+  }
+  auto total_cost = [&](const int* ww) {
+    int c = 0;
+    for (size_t i = 0; i < subs.size(); ++i)
+      c += best_choice(subs[i]->k, smem_bits[i], scol_bits[i], ww).cost;
+    return c;
+  };
+  int cost = total_cost(w);
+  const int ideal = [&] {
+    int c = 0;
+    for (const auto* sb : subs) c += sb->k == 2 ? 2 : 1;
+    return c;
+  }();
+  for (int sweep = 0; sweep < 4 && cost > ideal; ++sweep)
+    for (int j = 4; j < 10; ++j)
+      for (int v = 0; v < 8; ++v) {
+        const int old = w[j];
+        w[j] = v;
+        const int c = total_cost(w);
+        if (c < cost) cost = c;
+        else w[j] = old;
+      }
+  // placement: pieces sorted by G, piece at 16 * rank + G
+  int G[64], order[64];
+  for (int pi = 0; pi < 64; ++pi) {
+    int g = 0;
+    for (int b = 0; b < 6; ++b)
+      if ((pi >> b) & 1) g += w[4 + b];
+    G[pi] = g & 7;
+    order[pi] = pi;
+  }
+  std::stable_sort(order, order + 64, [&](int x, int y) { return G[x] < G[y]; });
+  int start_by_pidx[64];
+  for (int r = 0; r < 64; ++r) {
+    const int pi = order[r];
+    start_by_pidx[pi] = 16 * r + G[pi];
+    uint64_t off = 0;
+    for (int b = 0; b < 6; ++b)
+      if ((pi >> b) & 1) off += (uint64_t)1 << bpos[4 + b];
+    p.piece_goff[r] = off;
+    p.piece_start[r] = (uint16_t)start_by_pidx[pi];
+  }
+  for (int pi = 0; pi < 64; ++pi) p.start_by_pidx[pi] = (uint16_t)start_by_pidx[pi];
+  auto slot = [&](int idx) { return start_by_pidx[idx >> 4] + (idx & 15); };
+  for (int j = 0; j < 10; ++j) p.lo_mask[j] = ((uint64_t)1 << bpos[j]) - 1;
+  p.n_blocks = (uint64_t)1 << (s->L - 10);
+  p.mirror = use_mirror(s, op) ? 1u : 0u;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = std::getenv("TANQ_DBG");
+    dbg = e ? std::atoi(e) : 0;
+  }
+  p.dbg = (uint32_t)dbg;
+  p.n_sub = (int)subs.size();
+  // blob: per sub-op fragments then tables (both 16 B aligned)
+  size_t off = 0;
+  for (size_t i = 0; i < subs.size(); ++i) {
+    const FusedOp& sb = *subs[i];
+    tanq::BlockSub& g = p.sub[i];
+    g.k = sb.k;
+    const BlockSubChoice ch = best_choice(sb.k, smem_bits[i], scol_bits[i], w);
+    const std::vector<double2> Sm = member_order_S(sb, smap[i]);  // sub-op member order
+    // sub-op member bit t <-> block bit smem_bits[i][t]
+    auto sub_member = [&](const int* blkbits, int nb, int v) {  // value over blkbits -> member
+      int m = 0;
+      for (int b = 0; b < nb; ++b)
+        if ((v >> b) & 1) {
+          const int t = (int)(std::find(smem_bits[i].begin(), smem_bits[i].end(), blkbits[b]) -
+                              smem_bits[i].begin());
+          m |= 1 << t;
+        }
+      return m;
+    };
+    auto deposit = [&](const int* blkbits, int nb, int v) {
+      int idx = 0;
+      for (int b = 0; b < nb; ++b)
+        if ((v >> b) & 1) idx |= 1 << blkbits[b];
+      return idx;
+    };
+    // column bit order: n[0..2] first, then the rest ascending
+    std::vector<int> cols(ch.n, ch.n + 3);
+    for (int c : scol_bits[i])
+      if (std::find(cols.begin(), cols.end(), c) == cols.end()) cols.push_back(c);
+    g.a_off = (int)(off / 8);
+    uint16_t* T;
+    if (sb.k == 2) {
+      int in_bits[4] = {ch.k0, ch.k1, 0, 0}, out_bits[4] = {ch.o0, 0, 0, 0};
+      for (int t = 0, a = 2, b = 1; t < 4; ++t) {
+        const int bb = smem_bits[i][t];
+        if (bb != ch.k0 && bb != ch.k1) in_bits[a++] = bb;
+        if (bb != ch.o0) out_bits[b++] = bb;
+      }
+      double* F = reinterpret_cast<double*>(blob + off);
+      for (int mt = 0; mt < 2; ++mt)
+        for (int ks = 0; ks < 4; ++ks)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int row = mt * 8 + (lane >> 2), colk = ks * 4 + (lane & 3);
+            const double2 v = Sm[(size_t)sub_member(out_bits, 4, row) * 16 + sub_member(in_bits, 4, colk)];
+            const int e = (mt * 4 + ks) * 32 + lane;
+            F[0 * 256 + e] = v.x;
+            F[1 * 256 + e] = -(v.x + v.y);
+            F[2 * 256 + e] = v.y - v.x;
+          }
+      off += 768 * 8;
+      g.t_off = (int)(off / 2);
+      T = reinterpret_cast<uint16_t*>(blob + off);
+      for (int h = 0; h < 2; ++h)
+        for (int lane = 0; lane < 32; ++lane) {
+          uint16_t* t = T + (h * 32 + lane) * 32;
+          const int c4 = lane & 3, r4 = lane >> 2, hb = h << half;
+          for (int ks = 0; ks < 4; ++ks)
+            for (int j = 0; j < 4; ++j) {
+              const int idx = deposit(in_bits, 4, c4 | (ks << 2)) |
+                              deposit(cols.data(), (int)cols.size(), 8 * j + r4) | hb;
+              t[ks * 4 + j] = (uint16_t)slot(idx);
+            }
+          for (int mt = 0; mt < 2; ++mt)
+            for (int j = 0; j < 4; ++j)
+              for (int c = 0; c < 2; ++c) {
+                const int idx = deposit(out_bits, 4, r4 | (mt << 3)) |
+                                deposit(cols.data(), (int)cols.size(), 8 * j + 2 * c4 + c) | hb;
+                t[16 + (mt * 4 + j) * 2 + c] = (uint16_t)slot(idx);
+              }
+        }
+      off += 2 * 32 * 32 * 2;
+    } else {
+      double2* F = reinterpret_cast<double2*>(blob + off);
+      for (int e = 0; e < 16; ++e) F[e] = Sm[e];
+      off += 32 * 8;
+      g.t_off = (int)(off / 2);
+      T = reinterpret_cast<uint16_t*>(blob + off);
+      const int mbits[2] = {smem_bits[i][0], smem_bits[i][1]};  // member order = sorted position
+      for (int h = 0; h < 2; ++h)
+        for (int lane = 0; lane < 32; ++lane) {
+          uint16_t* t = T + (h * 32 + lane) * 16;
+          for (int j = 0; j < 4; ++j)
+            for (int m = 0; m < 4; ++m) {
+              const int idx = deposit(mbits, 2, m) |
+                              deposit(cols.data(), (int)cols.size(), lane + 32 * j) | (h << half);
+              t[j * 4 + m] = (uint16_t)slot(idx);
+            }
+        }
+      off += 2 * 32 * 16 * 2;
+    }
+  }
+  p.blob_bytes = (int)off;
+  p.pairs = block_pairs_for(off);
+  return off;
+}
+
 // Packed -> full layout (one pass), before anything that reads or writes elements the packed
 // layout does not keep up to date.
 tanq_status ensure_unpacked(tanq_sim* s) {
@@ -1063,13 +1375,14 @@ tanq_status ensure_unpacked(tanq_sim* s) {
 // Launch one fused op on every shard (targets must be local).  For k >= 3 (groups), `prog`
 // holds the group program already copied to each device (indexed like s->scratch).
 tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* gp,
-                      const std::vector<const double2*>* prog) {
+                      const std::vector<const double2*>* prog,
+                      const tanq::BlockParams* bp = nullptr) {
   const int k = op.k, M = 1 << (2 * k);
   const uint64_t n_tuples = (uint64_t)1 << (s->L - 2 * k);
   const double amps = (double)((uint64_t)1 << s->L);
   // algorithmic: 8 flops per complex MAC; executed: K1 (FMA) 8, K2 / K3 (3-multiply DMMA) 6
   double flops_amp = 8.0 * M, hw_amp = (k == 1 ? 8.0 : 6.0) * M;
-  if (gp && !op.sub.empty()) {
+  if ((gp || bp) && !op.sub.empty()) {
     flops_amp = hw_amp = 0;
     for (const auto& sb : op.sub) {
       const int Ms = 1 << (2 * sb.k);
@@ -1077,11 +1390,11 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       hw_amp += (sb.k == 1 ? 8.0 : 6.0) * Ms;
     }
   }
-  const bool mir_op = gp ? gp->mirror != 0 : use_mirror(s, op);
+  const bool mir_op = gp ? gp->mirror != 0 : (bp ? bp->mirror != 0 : use_mirror(s, op));
   if (!mir_op) TRY(ensure_unpacked(s));
   MemberMap mm;
   std::vector<double2> Sm;
-  if (!gp) {
+  if (!gp && !bp) {
     mm = member_map(s, k, op.q);
     Sm = member_order_S(op, mm);
   }
@@ -1094,13 +1407,19 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
     Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 16.0 : 32.0) * amps,
             fr * flops_amp * amps, fr * hw_amp * amps};
     prof_begin(s, sh, pr);
-    if (gp) {
+    if (gp || bp) {
       int di = 0;
       for (size_t i = 0; i < s->scratch.size(); ++i)
         if (s->scratch[i].device == sh.device) di = (int)i;
-      tanq::GroupParams p = *gp;
-      p.prog = (*prog)[di];
-      CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
+      if (bp) {
+        tanq::BlockParams p = *bp;
+        p.blob = (*prog)[di];
+        CUDA_TRY(tanq::launch_block_group(sh.data, p, sh.stream));
+      } else {
+        tanq::GroupParams p = *gp;
+        p.prog = (*prog)[di];
+        CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
+      }
     } else if (k == 1) {
       tanq::GateParams<1> p;
       std::memcpy(p.S, Sm.data(), sizeof(p.S));
@@ -1147,7 +1466,7 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   // into a persistent pinned host buffer and copied (async) to each device before the launch.
   size_t total = 0;
   for (const auto& op : ops)
-    if (op.k >= 2) total += group_prog_elems(op);  // k = 2: tiled or not, decided at launch
+    if (op.k >= 2) total += prog_capacity(op);  // k = 2: tiled or not, decided at launch
   if (total) {
     for (auto& sh : s->shards) {
       DevScratch& d = scratch_for(s, sh.device);
@@ -1166,15 +1485,23 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
   }
   size_t off = 0;
   tanq::GroupParams gp;
+  tanq::BlockParams bp;
   for (size_t i = 0; i < ops.size(); ++i) {
     const FusedOp& op = ops[i];
     TRY(ensure_local(s, op, &ops, i + 1));
-    if (!uses_prog(s, op)) {
+    const bool blk = block_ok(s, op);
+    if (!blk && !uses_prog(s, op)) {
       TRY(launch_op(s, op, nullptr, nullptr));
       continue;
     }
     double2* hp = s->frag_host + off;
-    build_group(s, op, gp, hp);
+    size_t elems;
+    if (blk) {
+      elems = (build_block(s, op, bp, reinterpret_cast<unsigned char*>(hp)) + 15) / 16;
+    } else {
+      build_group(s, op, gp, hp);
+      elems = gp.prog_elems;
+    }
     std::vector<const double2*> ptrs(s->scratch.size(), nullptr);
     for (auto& sh : s->shards) {
       int di = 0;
@@ -1183,13 +1510,16 @@ tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
       if (!ptrs[di]) {
         double2* dst = s->scratch[di].frag + off;
         CUDA_TRY(cudaSetDevice(sh.device));
-        CUDA_TRY(cudaMemcpyAsync(dst, hp, gp.prog_elems * sizeof(double2),
-                                 cudaMemcpyHostToDevice, sh.stream));
+        CUDA_TRY(cudaMemcpyAsync(dst, hp, elems * sizeof(double2), cudaMemcpyHostToDevice,
+                                 sh.stream));
         ptrs[di] = dst;
       }
     }
-    off += gp.prog_elems;
-    TRY(launch_op(s, op, &gp, &ptrs));
+    off += elems;
+    if (blk)
+      TRY(launch_op(s, op, nullptr, &ptrs, &bp));
+    else
+      TRY(launch_op(s, op, &gp, &ptrs));
   }
   if (total) {
     Shard& s0 = s->shards[0];
@@ -1560,8 +1890,12 @@ tanq_status tanq_create_dist(int n_qubits, int world_size, int rank, int device,
   return TANQ_OK;
 }
 
+tanq_status tanq_plan_destroy(tanq_plan* p);
+
 tanq_status tanq_destroy(tanq_sim* s) {
   if (!s) return TANQ_OK;
+  for (auto& e : s->plan_cache) tanq_plan_destroy(e.plan);
+  s->plan_cache.clear();
   for (auto& p : s->prof) {
     cudaEventDestroy(p.e0);
     cudaEventDestroy(p.e1);
@@ -1750,16 +2084,31 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     }
     size_t total = 0;
     for (const auto& op : p->ops)
-      if (op.k >= 2) total += group_prog_elems(op);  // upper bound (k = 2 may run direct)
+      if (op.k >= 2) total += prog_capacity(op);  // upper bound (k = 2 may run direct)
     std::vector<double2> host(total ? total : 1);
     std::vector<tanq::GroupParams> gps;
+    std::vector<tanq::BlockParams> bps;
+    std::vector<size_t> elems;
+    std::vector<int> kind;  // per op: 0 direct, 1 group, 2 block
     size_t off = 0;
     const bool herm_in = s->herm_state;
     for (const auto& op : p->ops) {  // the Hermitian flag as it will be when op runs
-      if (uses_prog(s, op)) {
+      if (block_ok(s, op)) {
+        bps.emplace_back();
+        const size_t e = (build_block(s, op, bps.back(), reinterpret_cast<unsigned char*>(
+                                                             host.data() + off)) + 15) / 16;
+        elems.push_back(e);
+        kind.push_back(2);
+        off += e;
+      } else if (uses_prog(s, op)) {
         gps.emplace_back();
         build_group(s, op, gps.back(), host.data() + off);
+        elems.push_back(gps.back().prog_elems);
+        kind.push_back(1);
         off += gps.back().prog_elems;
+      } else {
+        kind.push_back(0);
+        elems.push_back(0);
       }
       if (!op.herm) s->herm_state = false;
     }
@@ -1778,15 +2127,17 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     CUDA_TRY(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal));
     const uint64_t l0 = s->launches;
     off = 0;
-    size_t gi = 0;
+    size_t gi = 0, bi = 0;
     tanq_status st = TANQ_OK;
-    for (const auto& op : p->ops) {
-      if (!uses_prog(s, op)) {
+    for (size_t oi = 0; oi < p->ops.size(); ++oi) {
+      const FusedOp& op = p->ops[oi];
+      if (kind[oi] == 0) {
         st = launch_op(s, op, nullptr, nullptr);
       } else {
         ptr[di] = g.dprog + off;
-        off += gps[gi].prog_elems;
-        st = launch_op(s, op, &gps[gi++], &ptr);
+        off += elems[oi];
+        st = kind[oi] == 2 ? launch_op(s, op, nullptr, &ptr, &bps[bi++])
+                           : launch_op(s, op, &gps[gi++], &ptr);
       }
       if (st != TANQ_OK) break;
     }
@@ -1923,6 +2274,40 @@ tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* item
   return TANQ_OK;
 }
 
+// Instrumentation: the block-pipeline program of plan op i on a single-shard register in the
+// initial interleaved layout (packed = 1: the packed Hermitian layout), exactly as the launch
+// would build it.  *kind = 2 if the block kernel takes the op (params / blob written), else 0.
+tanq_status tanq_plan_block_program(const tanq_plan* p, uint64_t i, int packed, void* params,
+                                    size_t params_size, void* blob, size_t blob_cap, int* kind,
+                                    size_t* blob_bytes) {
+  if (!p || !kind) return fail(TANQ_E_ARG, "NULL argument");
+  if (i >= p->ops.size()) return fail(TANQ_E_ARG, "op index out of range");
+  tanq_sim shape;
+  shape.n = p->n;
+  shape.L = 2 * p->n;
+  for (int b = 0; b < 64; ++b) shape.phys[b] = (uint32_t)b;
+  shape.shards.resize(1);
+  shape.herm_state = true;
+  shape.mirror_allowed = packed != 0;
+  *kind = 0;
+  const FusedOp& op = p->ops[i];
+  if (!block_ok(&shape, op)) return TANQ_OK;
+  if (params_size != sizeof(tanq::BlockParams))
+    return fail(TANQ_E_ARG, "params_size mismatch (sizeof BlockParams)");
+  std::vector<unsigned char> tmp(block_blob_bytes(op) + 16);
+  tanq::BlockParams bp;
+  std::memset(&bp, 0, sizeof(bp));
+  const size_t bytes = build_block(&shape, op, bp, tmp.data());
+  if (blob_bytes) *blob_bytes = bytes;
+  if (blob) {
+    if (blob_cap < bytes) return fail(TANQ_E_ARG, "blob buffer too small");
+    std::memcpy(blob, tmp.data(), bytes);
+  }
+  if (params) std::memcpy(params, &bp, sizeof(bp));
+  *kind = 2;
+  return TANQ_OK;
+}
+
 tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits, tanq_c64* S) {
   if (!p || !k || !qubits) return fail(TANQ_E_ARG, "NULL argument");
   if (i >= p->ops.size()) return fail(TANQ_E_ARG, "op index out of range");
@@ -1981,12 +2366,104 @@ tanq_status tanq_plan_destroy(tanq_plan* p) {
   return TANQ_OK;
 }
 
+// tanq_run_circuit keeps the plans of the last kPlanCacheSize distinct (circuit, noise model,
+// options) it ran, keyed by an exact byte serialisation of everything the plan depends on
+// (ops with their matrix payloads, calibrations, fusion options) -- a repeated call skips
+// noise binding, superoperator construction and fusion.  From the second run of the same
+// single-shard plan on, its launches are replayed as one CUDA graph (flags bit1), unless
+// per-kernel profiling (bit0) is requested.  Env TANQ_PLAN_CACHE=0 disables the cache.
+namespace {
+constexpr size_t kPlanCacheSize = 8;
+
+void key_put(std::string& k, const void* p, size_t n) {
+  k.append(reinterpret_cast<const char*>(p), n);
+}
+
+bool plan_key(const tanq_sim* s, const tanq_circuit* c, const tanq_noise_model* nm,
+              const tanq_run_opts* o, std::string& k) {
+  if (!c || (c->n_ops && !c->ops)) return false;
+  k.clear();
+  k.reserve(64 + c->n_ops * 48);
+  key_put(k, &s->n, sizeof(s->n));
+  key_put(k, &s->L, sizeof(s->L));
+  tanq_run_opts opts{2, 3, 0, 0, 0};
+  if (o) opts = *o;
+  key_put(k, &opts.fuse, sizeof(opts.fuse));
+  key_put(k, &opts.k_max, sizeof(opts.k_max));
+  key_put(k, &opts.chunk_bytes, sizeof(opts.chunk_bytes));
+  key_put(k, &opts.flags, sizeof(opts.flags));
+  key_put(k, &c->n_ops, sizeof(c->n_ops));
+  for (uint64_t i = 0; i < c->n_ops; ++i) {
+    const tanq_op& op = c->ops[i];
+    key_put(k, &op.kind, sizeof(op.kind));
+    key_put(k, &op.k, sizeof(op.k));
+    key_put(k, op.q, sizeof(op.q));
+    key_put(k, &op.n_kraus, sizeof(op.n_kraus));
+    key_put(k, &op.theta, sizeof(op.theta));
+    if (op.m && op.k >= 1 && op.k <= 3) {
+      const size_t d = (size_t)1 << op.k;
+      size_t cnt = op.kind == TANQ_SUPEROP ? d * d * d * d
+                                           : (op.kind == TANQ_KRAUS ? (size_t)std::max(0, op.n_kraus) * d * d : d * d);
+      key_put(k, op.m, cnt * sizeof(tanq_c64));
+    }
+  }
+  const int has_nm = nm != nullptr;
+  key_put(k, &has_nm, sizeof(has_nm));
+  if (nm) {
+    if ((nm->n > 0 && !nm->qubits) || (nm->n_gates && !nm->gates)) return false;
+    key_put(k, &nm->n, sizeof(nm->n));
+    key_put(k, &nm->order, sizeof(nm->order));
+    if (nm->n > 0) key_put(k, nm->qubits, (size_t)nm->n * sizeof(tanq_qubit_cal));
+    key_put(k, &nm->n_gates, sizeof(nm->n_gates));
+    if (nm->n_gates) key_put(k, nm->gates, nm->n_gates * sizeof(tanq_gate_cal));
+  }
+  return true;
+}
+
+bool plan_cache_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TANQ_PLAN_CACHE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+}  // namespace
+
 tanq_status tanq_run_circuit(tanq_sim* s, const tanq_circuit* c, const tanq_noise_model* nm,
                              const tanq_run_opts* o, tanq_run_stats* st) {
-  tanq_plan* p = nullptr;
-  TRY(tanq_plan_create(s, c, nm, o, &p));
-  tanq_status r = tanq_plan_exec(s, p, st);
-  tanq_plan_destroy(p);
+  if (!s) return fail(TANQ_E_ARG, "NULL handle");
+  std::string key;
+  if (!plan_cache_on() || !plan_key(s, c, nm, o, key)) {
+    tanq_plan* p = nullptr;
+    TRY(tanq_plan_create(s, c, nm, o, &p));
+    tanq_status r = tanq_plan_exec(s, p, st);
+    tanq_plan_destroy(p);
+    return r;
+  }
+  PlanCacheEntry* hit = nullptr;
+  for (auto& e : s->plan_cache)
+    if (e.key == key) hit = &e;
+  if (!hit) {
+    tanq_plan* p = nullptr;
+    TRY(tanq_plan_create(s, c, nm, o, &p));
+    if (s->plan_cache.size() >= kPlanCacheSize) {  // evict the least recently used
+      auto lru = std::min_element(s->plan_cache.begin(), s->plan_cache.end(),
+                                  [](const PlanCacheEntry& a, const PlanCacheEntry& b) {
+                                    return a.last_use < b.last_use;
+                                  });
+      tanq_plan_destroy(lru->plan);
+      s->plan_cache.erase(lru);
+    }
+    s->plan_cache.push_back(PlanCacheEntry{std::move(key), p, 0, 0});
+    hit = &s->plan_cache.back();
+  } else {
+    hit->hits++;
+    if (hit->hits == 1 && !(hit->plan->flags & 1)) hit->plan->flags |= 2;  // replay as a graph
+  }
+  hit->last_use = ++s->plan_cache_clock;
+  tanq_status r = tanq_plan_exec(s, hit->plan, st);
+  if (st && hit->hits) st->plan_ms = 0.0;  // no planning on a cache hit
   return r;
 }
 

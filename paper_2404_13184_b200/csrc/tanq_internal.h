@@ -48,6 +48,32 @@ struct GroupParams {
   GroupSub sub[kMaxSub];
 };
 
+// Block-pipeline group kernel (tanq_block.cu).  A block = 10 physical bits (5 whole qubits in
+// the packed layout: the group's plus the lowest free ones), 64 pieces of 16 contiguous
+// amplitudes; a pair of warps streams blocks through two shared-memory stages.
+static constexpr int kBlockMaxPairs = 6;
+static constexpr int kBlockMaxSub = 12;
+struct BlockSub {
+  int32_t k;       // 1 or 2
+  int32_t a_off;   // doubles: k=2 fragments [3][2][4][32] (a, -(a+b), b-a); k=1: 16 double2
+  int32_t t_off;   // uint16: per-lane shared-memory offset tables [2 halves][32 lanes][32|16]
+};
+struct BlockParams {
+  const void* blob;          // sub-op fragments + offset tables (device), copied to shared
+  int32_t blob_bytes;        // multiple of 16
+  int32_t n_sub;
+  int32_t pairs;             // warp pairs per CTA (smem-limited, <= kBlockMaxPairs)
+  uint32_t mirror;           // packed Hermitian layout
+  uint32_t dbg;              // experiments only: 1 skip sub-ops, 2 skip HBM copies
+  uint32_t pad_;
+  uint64_t n_blocks;         // 2^(L - 10)
+  uint64_t lo_mask[10];      // (1 << pos) - 1 of the 10 block positions, ascending
+  uint64_t piece_goff[64];   // element offset of the piece handled by pair thread j
+  uint16_t piece_start[64];  // its shared-memory start (16 B units) in a stage
+  uint16_t start_by_pidx[64];// shared-memory start of piece index (block bits 4..9)
+  BlockSub sub[kBlockMaxSub];
+};
+
 struct BitMap {               // physical bit of each logical bit (row q -> 2q, col q -> 2q+1)
   uint32_t phys[64];
   int nbits;                 // 2n
@@ -57,6 +83,8 @@ struct BitMap {               // physical bit of each logical bit (row q -> 2q, 
 cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st);
 cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st);
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st);
+cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st);
+size_t block_smem_bytes(int pairs, int blob_bytes);
 // packed Hermitian layout -> full layout (single shard, interleaved identity bit map)
 cudaError_t launch_unpack(double2* a, int L, cudaStream_t st);
 size_t group_frag_elems(int k);                               // double2 per sub-op matrix

@@ -544,6 +544,7 @@ __device__ __forceinline__ void group_sub_k2(double2* X, const double2* F, const
         }
       }
     }
+    __syncwarp();  // every lane's B loads of this pass precede any lane's D stores
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll

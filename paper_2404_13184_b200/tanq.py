@@ -77,6 +77,20 @@ class tanq_run_stats(ctypes.Structure):
                 "plan_ms": self.plan_ms}
 
 
+class tanq_block_sub(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("a_off", ctypes.c_int32), ("t_off", ctypes.c_int32)]
+
+
+class tanq_block_params(ctypes.Structure):
+    """Mirror of tanq::BlockParams (csrc/tanq_internal.h) for tanq_plan_block_program."""
+    _fields_ = [("blob", ctypes.c_void_p), ("blob_bytes", ctypes.c_int32),
+                ("n_sub", ctypes.c_int32), ("pairs", ctypes.c_int32), ("mirror", ctypes.c_uint32),
+                ("dbg", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("n_blocks", ctypes.c_uint64), ("lo_mask", ctypes.c_uint64 * 10),
+                ("piece_goff", ctypes.c_uint64 * 64), ("piece_start", ctypes.c_uint16 * 64),
+                ("start_by_pidx", ctypes.c_uint16 * 64), ("sub", tanq_block_sub * 12)]
+
+
 class tanq_info(ctypes.Structure):
     _fields_ = [("n_qubits", ctypes.c_int32), ("n_shards", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
@@ -115,6 +129,8 @@ SIGNATURES = {
     "tanq_plan_info": ([_P, ctypes.POINTER(tanq_run_stats)], _I),
     "tanq_plan_get_op": ([_P, _U64, _P, _P, _P], _I),
     "tanq_plan_schedule": ([_P, _I, _P, _U64, ctypes.POINTER(_U64)], _I),
+    "tanq_plan_block_program": ([_P, _U64, _I, _P, ctypes.c_size_t, _P, ctypes.c_size_t,
+                                 ctypes.POINTER(_I), ctypes.POINTER(ctypes.c_size_t)], _I),
     "tanq_probs": ([_P, ctypes.POINTER(tanq_readout), _P], _I),
     "tanq_expect_pauli": ([_P, _U64, _U64, _P, _P], _I),
     "tanq_sample": ([_P, ctypes.POINTER(tanq_readout), _U64, _U64, _P], _I),
@@ -286,6 +302,22 @@ class Plan:
                    "tanq_plan_get_op")
             out.append((tuple(q[:k.value]), S))
         return out
+
+    def block_program(self, i: int, packed: bool = True):
+        """(params, blob bytes) of the block-pipeline kernel for op i, or None."""
+        prm = tanq_block_params()
+        kind, nbytes = ctypes.c_int(), ctypes.c_size_t()
+        _check(lib().tanq_plan_block_program(self.h, i, int(packed), ctypes.byref(prm),
+                                             ctypes.sizeof(prm), None, 0, ctypes.byref(kind),
+                                             ctypes.byref(nbytes)), "tanq_plan_block_program")
+        if kind.value != 2:
+            return None
+        blob = np.zeros(nbytes.value, dtype=np.uint8)
+        _check(lib().tanq_plan_block_program(self.h, i, int(packed), ctypes.byref(prm),
+                                             ctypes.sizeof(prm), blob.ctypes.data, blob.size,
+                                             ctypes.byref(kind), ctypes.byref(nbytes)),
+               "tanq_plan_block_program")
+        return prm, blob
 
     def close(self):
         if self.h:

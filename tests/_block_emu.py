@@ -1,0 +1,126 @@
+"""numpy emulation of the block-pipeline kernel's data movement (tanq_block.cu) from the program
+the host builds (tanq_plan_block_program): piece loads from in-place / transposed positions,
+the in-shared-memory transposition fixups, self-transposed blocks, every sub-op's fragment
+offset tables and A fragments, and the stores.  It checks the host-side program (placement,
+tables, fragment permutations, packed-layout decisions) on the CPU; the arithmetic order is not
+emulated (a complex matrix product stands in for the DMMA sequence).
+"""
+import numpy as np
+
+M55 = 0x5555555555555555
+
+
+def pair_swap(x: int) -> int:
+    return ((x & M55) << 1) | ((x >> 1) & M55)
+
+
+def pswap_bits(x: int, nbits: int) -> int:
+    m = int("01" * (nbits // 2), 2)
+    return ((x & m) << 1) | ((x >> 1) & m)
+
+
+def insert_zeros(t: int, lo_masks) -> int:
+    for m in lo_masks:
+        t = ((t & ~m) << 1) | (t & m)
+    return t
+
+
+def phys_of_rho(rho: np.ndarray, n: int) -> np.ndarray:
+    """a[P] with P's bit 2q = row bit q, bit 2q+1 = column bit q (initial interleaved layout)."""
+    N = 2 ** n
+    a = np.empty(N * N, dtype=np.complex128)
+    r = np.arange(N)
+    P_r = np.zeros(N, dtype=np.int64)
+    for q in range(n):
+        P_r |= ((r >> q) & 1) << (2 * q)
+    P_c = P_r << 1
+    a[(P_r[:, None] | P_c[None, :]).reshape(-1)] = rho.reshape(-1)
+    return a, P_r, P_c
+
+
+def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
+    """Run the block program on the physical-order state a (in place)."""
+    lo = [int(x) for x in prm.lo_mask]
+    goff = [int(x) for x in prm.piece_goff]
+    start = [int(x) for x in prm.piece_start]
+    sbp = [int(x) for x in prm.start_by_pidx]
+    mirror = bool(prm.mirror)
+    dbl = blob.view(np.float64)
+    u16 = blob.view(np.uint16)
+    assert sorted(start) == sorted(sbp)
+    for i in range(int(prm.n_blocks)):
+        if mirror and i > pair_swap(i):
+            continue
+        base = insert_zeros(i, lo)
+        self_t = mirror and pair_swap(base) == base
+        st = np.zeros(1032, dtype=np.complex128)
+        trs = []
+        for j in range(64):
+            e0 = base + goff[j]
+            em = pair_swap(e0)
+            tr = mirror and not self_t and e0 > em
+            src = em if tr else e0
+            st[start[j]:start[j] + 16] = a[src:src + 16]
+            trs.append((tr, src))
+            if tr:
+                piece = st[start[j]:start[j] + 16].copy()
+                for t in range(16):
+                    st[start[j] + pswap_bits(t, 4)] = np.conj(piece[t])
+        if self_t:
+            for idx in range(1024):
+                idm = pswap_bits(idx, 10)
+                if idx > idm:
+                    st[sbp[idx >> 4] + (idx & 15)] = np.conj(st[sbp[idm >> 4] + (idm & 15)])
+        for q in range(int(prm.n_sub)):
+            g = prm.sub[q]
+            for h in range(2):
+                if g.k == 2:
+                    F = dbl[g.a_off:g.a_off + 768].reshape(3, 2, 4, 32)
+                    a_ = F[0]
+                    b_ = F[2] + F[0]
+                    if check:
+                        assert np.allclose(F[1], -(a_ + b_), atol=1e-14, rtol=1e-14)
+                    S = np.zeros((16, 16), dtype=np.complex128)
+                    X = np.zeros((16, 32), dtype=np.complex128)
+                    rd, wr = [], []
+                    for lane in range(32):
+                        T = u16[g.t_off + (h * 32 + lane) * 32: g.t_off + (h * 32 + lane + 1) * 32]
+                        c4, r4 = lane & 3, lane >> 2
+                        for mt in range(2):
+                            for ks in range(4):
+                                S[mt * 8 + r4, ks * 4 + c4] = a_[mt, ks, lane] + 1j * b_[mt, ks, lane]
+                        for ks in range(4):
+                            for j in range(4):
+                                X[ks * 4 + c4, 8 * j + r4] = st[T[ks * 4 + j]]
+                                rd.append(int(T[ks * 4 + j]))
+                    Y = S @ X
+                    for lane in range(32):
+                        T = u16[g.t_off + (h * 32 + lane) * 32: g.t_off + (h * 32 + lane + 1) * 32]
+                        c4, r4 = lane & 3, lane >> 2
+                        for mt in range(2):
+                            for j in range(4):
+                                for c in range(2):
+                                    off = int(T[16 + (mt * 4 + j) * 2 + c])
+                                    st[off] = Y[8 * mt + r4, 8 * j + 2 * c4 + c]
+                                    wr.append(off)
+                    if check:
+                        assert len(set(rd)) == 512 and set(rd) == set(wr)
+                else:
+                    S = (dbl[g.a_off:g.a_off + 32].reshape(16, 2) @ np.array([1, 1j])).reshape(4, 4)
+                    rd = []
+                    for lane in range(32):
+                        T = u16[g.t_off + (h * 32 + lane) * 16: g.t_off + (h * 32 + lane + 1) * 16]
+                        for j in range(4):
+                            offs = [int(T[j * 4 + m]) for m in range(4)]
+                            rd += offs
+                            st[offs] = S @ st[offs]
+                    if check:
+                        assert len(set(rd)) == 512
+        for j in range(64):
+            tr, src = trs[j]
+            piece = st[start[j]:start[j] + 16].copy()
+            if tr:
+                for t in range(16):
+                    piece[pswap_bits(t, 4)] = np.conj(st[start[j] + t])
+            a[src:src + 16] = piece
+    return a

@@ -1,0 +1,102 @@
+"""Host-side program of the block-pipeline group kernel, checked on the CPU (-m "not gpu").
+
+tanq_plan_block_program exports exactly what a launch would use; tests/_block_emu.py replays
+its data movement in numpy (pieces, transposed loads, self-transposed blocks, offset tables,
+fragment permutations) and the result must equal the plan op's superoperator applied by the
+CPU oracle.  Also checks that the shared-memory placement makes the DMMA fragment accesses of
+3-qubit groups above qubit 1 bank-conflict free (8 distinct 16 B banks per quarter warp).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import dense
+
+from _block_emu import emulate, pair_swap, phys_of_rho
+
+
+@pytest.fixture(scope="module")
+def Plan():
+    from paper_2404_13184_b200.tanq import Plan
+    return Plan
+
+
+def _cases():
+    out = []
+    for n, seed in ((6, 1), (6, 2), (7, 3)):
+        c = W.random_circuit(n, 60, seed=5100 + seed, kmax=2, allow_matrix=True)
+        out.append((f"random{n}_{seed}", c, W.synthetic_calibration(c, seed, depol=True,
+                                                                    thermal=True, overrot=True)))
+    c, nm = W.config_workload(4, n=7)
+    out.append(("qpe7", c, nm))
+    c, nm = W.config_workload(3, n=6, depth=6)
+    out.append(("layered6", c, nm))
+    return out
+
+
+@pytest.mark.parametrize("name,circ,nm", _cases(), ids=[c[0] for c in _cases()])
+@pytest.mark.parametrize("packed", [True, False])
+def test_block_program_emulation_matches_oracle(Plan, name, circ, nm, packed):
+    plan = Plan(None, circ, nm, fuse=2, k_max=3)
+    ops = plan.ops()
+    n = circ.n
+    N = 2 ** n
+    rng = np.random.default_rng(hash(name) % 1000 + packed)
+    tested = 0
+    for i, (qs, S) in enumerate(ops):
+        prog = plan.block_program(i, packed=packed)
+        if prog is None:
+            continue
+        prm, blob = prog
+        assert prm.mirror == int(packed)
+        rho = (W.random_density(rng, n, rank=4) if packed
+               else W.random_complex(rng, (N, N)) * 0.1)
+        a, P_r, P_c = phys_of_rho(rho, n)
+        emulate(a, prm, blob)
+        ref = np.ascontiguousarray(rho.copy())
+        dense.apply_superop(ref, n, qs, S)
+        aref, _, _ = phys_of_rho(ref, n)
+        if packed:  # only the canonical element of each transpose pair is kept up to date
+            P = np.arange(N * N)
+            keep = np.array([p <= pair_swap(int(p)) for p in P])
+            d = np.abs(a[keep] - aref[keep]).max()
+        else:
+            d = np.abs(a - aref).max()
+        assert d < 1e-12, (name, i, qs, d)
+        tested += 1
+    assert tested >= 1
+
+
+def _bank_degrees(prm, blob):
+    """max lanes per 16 B bank over every quarter-warp of every fragment access."""
+    u16 = blob.view(np.uint16)
+    worst = []
+    for q in range(prm.n_sub):
+        g = prm.sub[q]
+        if g.k != 2:
+            continue
+        for h in range(2):
+            T = np.array([u16[g.t_off + (h * 32 + l) * 32: g.t_off + (h * 32 + l + 1) * 32]
+                          for l in range(32)])               # [lane][32]
+            for e in range(32):
+                for ph in range(4):
+                    banks = T[8 * ph: 8 * ph + 8, e] % 8
+                    worst.append(np.bincount(banks, minlength=8).max())
+    return max(worst) if worst else 1
+
+
+def test_block_layout_bank_conflict_free(Plan):
+    """QPE groups (3 qubits, all above qubit 1): every B / D fragment quarter-warp hits 8
+    distinct banks."""
+    c, nm = W.config_workload(4, n=8)
+    plan = Plan(None, c, nm, fuse=2, k_max=3)
+    seen = 0
+    for i, (qs, S) in enumerate(plan.ops()):
+        if min(qs) < 2:
+            continue
+        prog = plan.block_program(i, packed=True)
+        if prog is None:
+            continue
+        assert _bank_degrees(*prog) == 1, (i, qs)
+        seen += 1
+    assert seen >= 3

@@ -452,3 +452,39 @@ def test_packed_layout_transitions(Sim):
         plan2.exec(sim)                                 # starts unpacked: recapture
         ref3 = dense.run(c, nm, rho=np.ascontiguousarray(ref2.copy()))
         assert_parity(rho_of(sim, n), ref3)
+
+
+def test_run_circuit_plan_cache(Sim):
+    """tanq_run_circuit caches plans by an exact key (ops, payloads, calibration, options):
+    repeated runs replay the cached plan (as a CUDA graph from the second run), and any change
+    of a matrix payload or calibration number plans afresh."""
+    n = 6
+    c = W.random_circuit(n, 50, seed=4242, kmax=3)
+    nm = W.synthetic_calibration(c, 4242, depol=True, thermal=True, overrot=True)
+    ref = dense.run(c, nm)
+    with Sim(n) as sim:
+        for it in range(4):
+            sim.reset()
+            st = sim.run_circuit(c, nm)
+            assert_parity(rho_of(sim, n), ref)
+            if it:
+                assert st["plan_ms"] == 0.0
+        # a different calibration value -> a different plan
+        key = next(iter(nm.gates))
+        nm.gates[key].depol_p *= 0.5
+        ref2 = dense.run(c, nm)
+        sim.reset()
+        st = sim.run_circuit(c, nm)
+        assert st["plan_ms"] > 0.0
+        assert_parity(rho_of(sim, n), ref2)
+        # a different user matrix payload (same shapes) -> a different plan
+        i = next(j for j, o in enumerate(c.ops) if o.kind in ("u", "kraus"))
+        op = c.ops[i]
+        if op.kind == "u":
+            op.mat = op.mat @ np.diag(np.exp(1j * np.arange(op.mat.shape[0])))
+        else:
+            op.kraus = [K * np.exp(0.3j) for K in op.kraus]
+        ref3 = dense.run(c, nm)
+        sim.reset()
+        sim.run_circuit(c, nm)
+        assert_parity(rho_of(sim, n), ref3)

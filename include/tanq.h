@@ -294,6 +294,22 @@ tanq_status tanq_qasm_circuit(const tanq_qasm* q, tanq_circuit* c, int* n_qubits
 tanq_status tanq_qasm_measures(const tanq_qasm* q, int32_t* qubit_of_clbit);
 tanq_status tanq_qasm_free(tanq_qasm* q);
 
+/* ---- device calibration (NEXT-4; Sec. 3.5; schema SPEC S:365-370) -------
+ * { "name", "num_qubits", "qubits": [{"t1_us", "t2_us", "prob_meas0_prep1",
+ *   "prob_meas1_prep0", "frequency_ghz"?, "readout_length_ns"?}], "gates": [{"name": id|sx|x|
+ *   rz|cx, "qubits": [q] | [c, t], "error", "duration_ns", "overrot_rad"?}], "coupling_map"? }
+ * Gate error e -> depolarizing p = e d/(d-1), d = 2^k, clamped to 1 (reading R6); RZ entries
+ * ignored (noiseless); T2 > 2 T1 rejected.  TANQ_E_ARG names the JSON path at fault. */
+typedef struct tanq_device tanq_device;
+tanq_status tanq_device_parse(const char* json, tanq_device** out);
+/* The noise model of the device (order 0); its arrays stay owned by the tanq_device and
+ * valid until tanq_device_free.  *n_qubits (nullable) = num_qubits. */
+tanq_status tanq_device_noise(const tanq_device* d, tanq_noise_model* nm, int* n_qubits);
+/* coupling_map pairs (2 int32 each); pairs = NULL queries the count. */
+tanq_status tanq_device_coupling(const tanq_device* d, int32_t* pairs, uint64_t max, uint64_t* n);
+const char* tanq_device_name(const tanq_device* d);
+tanq_status tanq_device_free(tanq_device* d);
+
 /* ---- instrumentation -------------------------------------------------------------- */
 /* Copy up to max entries of the per-kernel profile; returns count in *n_out. */
 tanq_status tanq_profile_read(tanq_sim* s, tanq_kernel_prof* out, int max, int* n_out);

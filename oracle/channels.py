@@ -166,3 +166,27 @@ def gate_channel_sequence(op, noise) -> List[tuple]:
 def readout_matrix(p10: float, p01: float) -> np.ndarray:
     """Column-stochastic confusion M = [[1-P(1|0), P(0|1)], [P(1|0), 1-P(0|1)]] (R11)."""
     return np.array([[1 - p10, p01], [p10, 1 - p01]])
+
+
+def noise_model_from_device(dev: dict):
+    """Oracle-side reading of a device-calibration snapshot (SPEC S:365-370 schema; the
+    paper's calibration-driven noise, Sec. 3.5): per qubit T1, T2 and readout
+    P(0|1), P(1|0); per (gate, qubits) a depolarizing parameter from the reported gate error
+    e as p = e d / (d - 1), d = 2^k (reading R6: e is the average infidelity of a
+    d-dimensional depolarizing channel, F_avg = 1 - p (d - 1) / d), clamped to 1, and the
+    gate duration for thermal relaxation; RZ noiseless (R9).  Written independently of the
+    library's C++ parser."""
+    import workloads as W  # data classes only
+    n = int(dev["num_qubits"])
+    qubits = [W.QubitCal(float(q["t1_us"]), float(q["t2_us"]), float(q["prob_meas1_prep0"]),
+                         float(q["prob_meas0_prep1"])) for q in dev["qubits"]]
+    nm = W.NoiseModel(n, qubits)
+    for g in dev["gates"]:
+        if g["name"] == "rz":
+            continue
+        qs = tuple(int(x) for x in g["qubits"])
+        d = 2 ** len(qs)
+        p = min(1.0, float(g["error"]) * d / (d - 1))
+        nm.gates[(g["name"], qs)] = W.GateCal(p, float(g["duration_ns"]),
+                                              float(g.get("overrot_rad", 0.0)))
+    return nm

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtanq.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("tanq_host.cpp", "tanq_kernels.cu", "tanq_block.cu", "tanq_qasm.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("tanq_host.cpp", "tanq_kernels.cu", "tanq_block.cu", "tanq_qasm.cpp",
+                                             "tanq_device.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "tanq_internal.h"), os.path.join(ROOT, "include", "tanq.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

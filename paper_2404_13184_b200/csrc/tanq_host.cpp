@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -50,6 +51,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;  // optional
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                        // optional
 };
 
 NcclApi& nccl() {
@@ -73,6 +76,8 @@ NcclApi& nccl() {
   LOAD(Recv);
   LOAD(AllReduce);
   LOAD(GetErrorString);
+  LOAD(CommGetAsyncError);
+  LOAD(CommAbort);
 #undef LOAD
   api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart &&
            api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.GetErrorString;
@@ -618,11 +623,13 @@ void reset_layout(tanq_sim* s) {
   for (int i = 0; i < 64; ++i) s->phys[i] = (uint32_t)i;  // rowpos(q)=2q, colpos(q)=2q+1
 }
 
+tanq_status host_wait(tanq_sim* s, cudaStream_t st);
+
 // wait for all shards' streams (cross-stream / cross-device ordering point)
 tanq_status join_all(tanq_sim* s) {
   for (auto& sh : s->shards) {
     CUDA_TRY(cudaSetDevice(sh.device));
-    CUDA_TRY(cudaStreamSynchronize(sh.stream));
+    TRY(host_wait(s, sh.stream));
   }
   return TANQ_OK;
 }
@@ -672,6 +679,61 @@ tanq_status ensure_unpacked(tanq_sim* s);
 // Ordering: comm(i) waits pack(i) (event xev_pack[j]); unpack(i) waits comm(i) (xev_comm[j]);
 // pack(i+2) reuses slot j after unpack(i) on S, so slot reuse is ordered by S itself.
 // In place: pack(i) reads chunk i of the outgoing part before unpack(i) overwrites it (S order).
+// Host wait for a stream.  Multi-process handles poll instead of blocking: every NCCL call is
+// asynchronous, so a peer that died or a broken link shows up only as a stream that never
+// completes (the paper saw fine-grained remote access hang the fabric).  The poll
+// checks ncclCommGetAsyncError and gives up after TANQ_NCCL_TIMEOUT_S seconds (default 600),
+// aborting the communicator and returning TANQ_E_NCCL instead of hanging the process.
+tanq_status host_wait(tanq_sim* s, cudaStream_t st) {
+  if (!s->comm) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return TANQ_OK;
+  }
+  static double timeout_s = -1;
+  if (timeout_s < 0) {
+    const char* e = getenv("TANQ_NCCL_TIMEOUT_S");
+    timeout_s = e ? std::atof(e) : 600.0;
+    if (timeout_s <= 0) timeout_s = 600.0;
+  }
+  cudaEvent_t ev;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t ce = cudaEventRecord(ev, st);
+  if (ce != cudaSuccess) {
+    cudaEventDestroy(ev);
+    return fail(TANQ_E_CUDA, std::string("cudaEventRecord -> ") + cudaGetErrorString(ce));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned it = 0;; ++it) {
+    ce = cudaEventQuery(ev);
+    if (ce == cudaSuccess) break;
+    if (ce != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      return fail(TANQ_E_CUDA, std::string("stream wait -> ") + cudaGetErrorString(ce));
+    }
+    ncclResult_t ar = ncclSuccess;
+    if (nccl().CommGetAsyncError && nccl().CommGetAsyncError(s->comm, &ar) == ncclSuccess &&
+        ar != ncclSuccess && ar != ncclInProgress) {
+      cudaEventDestroy(ev);
+      if (nccl().CommAbort) nccl().CommAbort(s->comm);
+      s->comm = nullptr;
+      return fail(TANQ_E_NCCL, std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ar));
+    }
+    const double el =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > timeout_s) {
+      cudaEventDestroy(ev);
+      if (nccl().CommAbort) nccl().CommAbort(s->comm);
+      s->comm = nullptr;
+      return fail(TANQ_E_NCCL, "stream did not complete within TANQ_NCCL_TIMEOUT_S (" +
+                                   std::to_string(timeout_s) + " s): peer or link failure; "
+                                   "communicator aborted");
+    }
+    if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  cudaEventDestroy(ev);
+  return TANQ_OK;
+}
+
 template <class Pack, class Unpack>
 tanq_status exchange_pipelined(tanq_sim* s, Shard& sh, int peer, uint64_t total, Pack pack,
                                Unpack unpack) {
@@ -1714,7 +1776,7 @@ tanq_status combine_probs(tanq_sim* s, DevScratch*& primary) {
       if (sh.device == d->device) st = sh.stream;
     CUDA_TRY(cudaSetDevice(d->device));
     CUDA_TRY(cudaMemcpyAsync(&bits, d->imax, sizeof(bits), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    TRY(host_wait(s, st));
     double v;
     std::memcpy(&v, &bits, sizeof(v));
     imx = std::max(imx, v);
@@ -1969,7 +2031,7 @@ tanq_status tanq_set_stream(tanq_sim* s, int shard, void* stream) {
   if (!s || shard < 0 || shard >= (int)s->shards.size()) return fail(TANQ_E_ARG, "bad shard");
   Shard& sh = s->shards[shard];
   CUDA_TRY(cudaSetDevice(sh.device));
-  CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  TRY(host_wait(s, sh.stream));
   cudaStream_t ns = stream ? (cudaStream_t)stream : s->own_streams_of(sh.device);
   for (auto& o : s->shards)
     if (o.device == sh.device) o.stream = ns;
@@ -2486,7 +2548,7 @@ tanq_status tanq_probs(tanq_sim* s, const tanq_readout* ro, double* probs) {
   }
   CUDA_TRY(cudaMemcpyAsync(probs, pd->probs, sizeof(double) << s->n, cudaMemcpyDeviceToHost,
                            s0.stream));
-  CUDA_TRY(cudaStreamSynchronize(s0.stream));
+  TRY(host_wait(s, s0.stream));
   return TANQ_OK;
 }
 
@@ -2513,7 +2575,7 @@ tanq_status tanq_expect_pauli(tanq_sim* s, uint64_t xm, uint64_t zm, double* out
       NCCL_TRY(nccl().AllReduce(d.scal, d.scal, 2, ncclDouble, ncclSum, s->comm, sh.stream));
     CUDA_TRY(cudaMemcpyAsync(&host[i], d.scal, sizeof(double2), cudaMemcpyDeviceToHost,
                              sh.stream));
-    CUDA_TRY(cudaStreamSynchronize(sh.stream));
+    TRY(host_wait(s, sh.stream));
   }
   for (auto& v : host) {
     re += v.x;
@@ -2551,7 +2613,7 @@ tanq_status tanq_sample(tanq_sim* s, const tanq_readout* ro, uint64_t seed, uint
   CUDA_TRY(cudaMemcpyAsync(outcomes, dout, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                            s0.stream));
   CUDA_TRY(cudaFreeAsync(dout, s0.stream));
-  CUDA_TRY(cudaStreamSynchronize(s0.stream));
+  TRY(host_wait(s, s0.stream));
   return TANQ_OK;
 }
 
@@ -2617,7 +2679,7 @@ static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c6
         CUDA_TRY(tanq::launch_scatter_vec(sh.data, d.stage, bm, s->n, s->L, (uint64_t)sh.id,
                                           first + off, cnt, sh.stream));
         s->launches++;
-        CUDA_TRY(cudaStreamSynchronize(sh.stream));
+        TRY(host_wait(s, sh.stream));
       }
       continue;
     }
@@ -2636,7 +2698,7 @@ static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c6
                                  sh.stream));
         CUDA_TRY(cudaMemcpyAsync(tmp.data(), d.stage, cnt * sizeof(double2),
                                  cudaMemcpyDeviceToHost, sh.stream));
-        CUDA_TRY(cudaStreamSynchronize(sh.stream));
+        TRY(host_wait(s, sh.stream));
         for (uint64_t i = 0; i < cnt; ++i) {  // exactly one shard owns each entry: x + 0
           acc[i].x += tmp[i].x;
           acc[i].y += tmp[i].y;
@@ -2655,7 +2717,7 @@ static tanq_status state_io(tanq_sim* s, uint64_t first, uint64_t count, tanq_c6
       for (auto& sh : s->shards) TRY(stream_wait(s0, sh));  // every shard's gather lands first
       CUDA_TRY(cudaMemcpyAsync(out + off, d.stage, cnt * sizeof(double2), cudaMemcpyDeviceToHost,
                                s0.stream));
-      CUDA_TRY(cudaStreamSynchronize(s0.stream));
+      TRY(host_wait(s, s0.stream));
     }
   }
   return TANQ_OK;
@@ -2694,7 +2756,7 @@ tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm) {
   s->launches++;
   unsigned long long h[2];
   CUDA_TRY(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, sh.stream));
-  CUDA_TRY(cudaStreamSynchronize(sh.stream));
+  TRY(host_wait(s, sh.stream));
   double diff, mx;
   std::memcpy(&diff, &h[0], sizeof(double));
   std::memcpy(&mx, &h[1], sizeof(double));

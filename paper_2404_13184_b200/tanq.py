@@ -140,6 +140,11 @@ SIGNATURES = {
     "tanq_qasm_measures": ([_P, _P], _I),
     "tanq_qasm_free": ([_P], _I),
     "tanq_check_hermitian": ([_P, _D, ctypes.POINTER(_I)], _I),
+    "tanq_device_parse": ([ctypes.c_char_p, ctypes.POINTER(_P)], _I),
+    "tanq_device_noise": ([_P, ctypes.POINTER(tanq_noise_model), ctypes.POINTER(_I)], _I),
+    "tanq_device_coupling": ([_P, _P, _U64, ctypes.POINTER(_U64)], _I),
+    "tanq_device_name": ([_P], ctypes.c_char_p),
+    "tanq_device_free": ([_P], _I),
     "tanq_get_state": ([_P, _U64, _U64, _P], _I),
     "tanq_set_state": ([_P, _U64, _U64, _P], _I),
     "tanq_sync": ([_P], _I),
@@ -254,7 +259,7 @@ class Plan:
     def __init__(self, sim, circuit, noise=None, *, fuse=2, k_max=3, profile=False,
                  world_size: int = 1, graph: bool = False, mirror: bool = True):
         cc = CCircuit(circuit.ops)
-        cn = CNoise(noise) if noise is not None else None
+        cn = _noise_of(noise)
         opts = tanq_run_opts(fuse, k_max, 0,
                              (1 if profile else 0) | (2 if graph else 0) | (0 if mirror else 4), 0)
         h = ctypes.c_void_p()
@@ -267,8 +272,12 @@ class Plan:
             _check(lib().tanq_plan_create(sim.h, ctypes.byref(cc.c), nmp, ctypes.byref(opts),
                                           ctypes.byref(h)), "tanq_plan_create")
         self.h = h
-        self.h2d_bytes = ctypes.sizeof(cc.arr) + sum(a.nbytes for a in cc.keep) + (
-            ctypes.sizeof(cn.qa) + ctypes.sizeof(cn.ga) if cn is not None else 0)
+        nb = 0
+        if isinstance(cn, CNoise):
+            nb = ctypes.sizeof(cn.qa) + ctypes.sizeof(cn.ga)
+        elif cn is not None:
+            nb = cn.c.n * ctypes.sizeof(tanq_qubit_cal) + cn.c.n_gates * ctypes.sizeof(tanq_gate_cal)
+        self.h2d_bytes = ctypes.sizeof(cc.arr) + sum(a.nbytes for a in cc.keep) + nb
 
     def exec(self, sim: "Simulator") -> dict:
         st = tanq_run_stats()
@@ -374,6 +383,59 @@ class QasmCircuit:
             pass
 
 
+class Device:
+    """tanq_device_parse: a device-calibration JSON (T1, T2, readout, gate error and length;
+    SPEC S:365-370 schema) -> the library's noise model.  Pass it wherever a noise model is
+    accepted; `.readout()` gives the per-qubit readout confusion for probs / sample."""
+
+    def __init__(self, text: str):
+        h = ctypes.c_void_p()
+        _check(lib().tanq_device_parse(text.encode(), ctypes.byref(h)), "tanq_device_parse")
+        self.h = h
+        self.c = tanq_noise_model()
+        n = ctypes.c_int()
+        _check(lib().tanq_device_noise(h, ctypes.byref(self.c), ctypes.byref(n)),
+               "tanq_device_noise")
+        self.n = n.value
+        self.name = lib().tanq_device_name(h).decode()
+        cnt = ctypes.c_uint64()
+        _check(lib().tanq_device_coupling(h, None, 0, ctypes.byref(cnt)), "tanq_device_coupling")
+        pairs = np.zeros(2 * max(1, cnt.value), dtype=np.int32)
+        _check(lib().tanq_device_coupling(h, pairs.ctypes.data, cnt.value, ctypes.byref(cnt)),
+               "tanq_device_coupling")
+        self.coupling = [tuple(int(x) for x in pairs[2 * i:2 * i + 2]) for i in range(cnt.value)]
+
+    def gates(self):
+        """[(kind name, qubits, depol_p, duration_ns, overrot_rad)] as bound by the library."""
+        names = {v: k for k, v in KIND.items()}
+        out = []
+        for i in range(self.c.n_gates):
+            g = self.c.gates[i]
+            out.append((names[g.kind], tuple(g.q[:g.k]), g.depol_p, g.duration_ns, g.overrot_rad))
+        return out
+
+    def readout(self) -> "CReadout":
+        return CReadout([self.c.qubits[q].p_meas1_prep0 for q in range(self.n)],
+                        [self.c.qubits[q].p_meas0_prep1 for q in range(self.n)])
+
+    def close(self):
+        if self.h:
+            lib().tanq_device_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _noise_of(noise):
+    if noise is None:
+        return None
+    return noise if isinstance(noise, Device) else CNoise(noise)
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().tanq_nccl_unique_id(buf, 128), "tanq_nccl_unique_id")
@@ -474,7 +536,7 @@ class Simulator:
             cc = _C()
         else:
             cc = prepared[0] if prepared else CCircuit(circuit.ops)
-        cn = (prepared[1] if prepared else (CNoise(noise) if noise is not None else None))
+        cn = prepared[1] if prepared else _noise_of(noise)
         opts = tanq_run_opts(fuse, k_max, 0, (1 if profile else 0) | (0 if mirror else 4), 0)
         st = tanq_run_stats()
         _check(lib().tanq_run_circuit(self.h, ctypes.byref(cc.c),
@@ -489,7 +551,7 @@ class Simulator:
 
     @staticmethod
     def prepare(circuit, noise=None):
-        return (CCircuit(circuit.ops), CNoise(noise) if noise is not None else None)
+        return (CCircuit(circuit.ops), _noise_of(noise))
 
     # -- reductions -----------------------------------------------------------------
     def probs(self, readout=None) -> np.ndarray:

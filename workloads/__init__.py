@@ -365,6 +365,42 @@ def cluster_product_workload(n: int, clusters: Sequence[Sequence[int]], layers: 
     return circ, nm, [(tuple(cl),) + restrict(circ, nm, cl) for cl in clusters]
 
 
+# 16-qubit heavy-hex coupling of the Falcon r4P devices (ibmq_guadalupe), as pairs
+GUADALUPE_COUPLING = [(0, 1), (1, 2), (1, 4), (2, 3), (3, 5), (4, 7), (5, 8), (6, 7), (7, 10),
+                      (8, 9), (8, 11), (10, 12), (11, 14), (12, 13), (12, 15), (13, 14)]
+
+
+def synthetic_device(n: int = 16, seed: int = BASE_SEED + 99, coupling=None,
+                     name: str = "synthetic_guadalupe_like") -> dict:
+    """A device-calibration snapshot in the JSON schema of SPEC S:365-370 with the synthetic
+    calibration ranges of the input recipe: T1/T2, readout P(0|1)/P(1|0),
+    per-gate error and duration for id/sx/x on every qubit, cx on both directions of every
+    coupled pair, rz listed as noiseless.  Numbers only -- the error -> depolarizing
+    conversion belongs to each side (library: tanq_device.cpp; oracle: channels.py)."""
+    rng = np.random.default_rng(seed)
+    coupling = list(coupling if coupling is not None else GUADALUPE_COUPLING)
+    qubits = []
+    for _ in range(n):
+        t1 = float(rng.uniform(50.0, 150.0))
+        t2 = float(min(rng.uniform(0.4, 1.2) * t1, 2.0 * t1))
+        qubits.append({"t1_us": t1, "t2_us": t2, "frequency_ghz": float(rng.uniform(4.9, 5.3)),
+                       "readout_length_ns": 5351.1,
+                       "prob_meas0_prep1": float(rng.uniform(0.01, 0.06)),
+                       "prob_meas1_prep0": float(rng.uniform(0.005, 0.03))})
+    gates = []
+    for q in range(n):
+        for g in ("id", "sx", "x"):
+            gates.append({"name": g, "qubits": [q], "error": float(rng.uniform(1e-4, 5e-4)),
+                          "duration_ns": 35.5})
+        gates.append({"name": "rz", "qubits": [q], "error": 0.0, "duration_ns": 0.0})
+    for a, b in coupling:
+        for c, t in ((a, b), (b, a)):
+            gates.append({"name": "cx", "qubits": [c, t], "error": float(rng.uniform(5e-3, 2e-2)),
+                          "duration_ns": float(rng.uniform(250.0, 550.0))})
+    return {"name": name, "num_qubits": n, "qubits": qubits, "gates": gates,
+            "coupling_map": [list(p) for p in coupling]}
+
+
 CONFIGS = {
     1: "3-qubit GHZ + depolarizing gate noise + readout (paper worked example)",
     2: "10-qubit QFT, thermal relaxation + coherent over-rotation",

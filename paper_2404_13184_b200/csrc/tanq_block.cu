@@ -81,6 +81,19 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// arrive on the mbarrier once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -123,24 +136,26 @@ __device__ __forceinline__ void piece_transpose(double2* P, int rot) {
   for (int i = 0; i < 16; ++i) P[pswap4((i + rot) & 15)] = make_double2(v[i].x, -v[i].y);
 }
 
-// k = 2 sub-op on one warp's half block.  F: fragments [3][2 mt][4 ks][32 lanes] doubles
+// k = 2 sub-op on one warp's half block.  F: fragments [3][4 ks][32 lanes][2 mt] doubles
 // (a, -(a+b), b-a); T: this lane's 32 offsets (16 B-fragment [ks][j], 16 D-fragment [mt][j][c]).
 template <int UI>
 __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const uint16_t* T,
-                                           int lane) {
+                                           int lane, int trow, int rows) {
   double a1[2][4], a2[2][4], a3[2][4];
+  const double2* F2 = reinterpret_cast<const double2*>(F);  // [mat][ks][lane] = (mt 0, mt 1)
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      a1[mt][ks] = F[(0 * 8 + mt * 4 + ks) * 32 + lane];
-      a2[mt][ks] = F[(1 * 8 + mt * 4 + ks) * 32 + lane];
-      a3[mt][ks] = F[(2 * 8 + mt * 4 + ks) * 32 + lane];
-    }
+  for (int ks = 0; ks < 4; ++ks) {
+    const double2 v1 = F2[(0 * 4 + ks) * 32 + lane], v2 = F2[(1 * 4 + ks) * 32 + lane],
+                  v3 = F2[(2 * 4 + ks) * 32 + lane];
+    a1[0][ks] = v1.x; a1[1][ks] = v1.y;
+    a2[0][ks] = v2.x; a2[1][ks] = v2.y;
+    a3[0][ks] = v3.x; a3[1][ks] = v3.y;
+  }
   uint32_t ob[8], od[8];  // packed uint16 pairs
-  {
+  {  // table [4 chunks][rows][8 uint16]: a quarter warp reads 8 consecutive 16 B chunks
     const uint4* t4 = reinterpret_cast<const uint4*>(T);
-    const uint4 b0 = t4[0], b1 = t4[1], d0 = t4[2], d1 = t4[3];
+    const uint4 b0 = t4[trow], b1 = t4[rows + trow], d0 = t4[2 * rows + trow],
+                d1 = t4[3 * rows + trow];
     ob[0] = b0.x; ob[1] = b0.y; ob[2] = b0.z; ob[3] = b0.w;
     ob[4] = b1.x; ob[5] = b1.y; ob[6] = b1.z; ob[7] = b1.w;
     od[0] = d0.x; od[1] = d0.y; od[2] = d0.z; od[3] = d0.w;
@@ -203,12 +218,13 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
 }
 
 // k = 1 sub-op (4x4 complex, DFMA): T = this lane's 16 offsets [j column][i member].
-__device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const uint16_t* T) {
+__device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const uint16_t* T,
+                                           int trow, int rows) {
   const double2* S = reinterpret_cast<const double2*>(F);
   uint32_t o[8];
-  {
+  {  // table [2 chunks][rows][8 uint16]
     const uint4* t4 = reinterpret_cast<const uint4*>(T);
-    const uint4 a = t4[0], b = t4[1];
+    const uint4 a = t4[trow], b = t4[rows + trow];
     o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
     o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
   }
@@ -240,21 +256,35 @@ __device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const ui
 }  // namespace
 
 constexpr int kStageUnits = 1032;  // 16 x 64 + rotation slack (<= 7), rounded to 8 units
+// shared header: mbarriers [2 * kBlockMaxPairs], piece offsets [64] (u64), starts [64] (u16)
+constexpr int kBlockHdrBytes = 768;
+static_assert(16 * kBlockMaxPairs + 64 * 8 + 64 * 2 <= kBlockHdrBytes, "block header");
 
-template <int UI>
+// COPY = 0: every pair thread moves one 256 B piece with cp.async.bulk (G2S with mbarrier
+// complete_tx, S2G bulk_group).  COPY = 1: the pair's 64 threads move the block as 16 B
+// cp.async.cg copies (16 per thread, 16 lanes per piece: every warp instruction reads two
+// contiguous 256 B runs), signalled with cp.async.mbarrier.arrive, and store it back with
+// coalesced LDS + STG.128 -- no per-lane serialised bulk-copy issue.
+template <int UI, int COPY>
 __global__ void __launch_bounds__(384, 1)
     block_kernel(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);  // [2 * kMaxPairs]
-  unsigned char* sBlob = smem_raw + 16 * kBlockMaxPairs;
+  uint64_t* sGoff = mbar + 2 * kBlockMaxPairs;              // [64] piece offsets by rank
+  uint16_t* sStart = reinterpret_cast<uint16_t*>(sGoff + 64);  // [64] piece starts by rank
+  unsigned char* sBlob = smem_raw + kBlockHdrBytes;
   double2* sStage = reinterpret_cast<double2*>(sBlob + p.blob_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1, pt = threadIdx.x & 63;
 
-  {  // blob (sub-op fragments + offset tables) -> shared; mbarrier init
+  {  // blob (sub-op fragments + offset tables) -> shared; piece tables; mbarrier init
     const uint4* src = reinterpret_cast<const uint4*>(p.blob);
     uint4* dst = reinterpret_cast<uint4*>(sBlob);
     for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x < 64) {
+      sGoff[threadIdx.x] = p.piece_goff[threadIdx.x];
+      sStart[threadIdx.x] = p.piece_start[threadIdx.x];
+    }
     if (threadIdx.x < 2 * p.pairs) mbar_init(&mbar[threadIdx.x], 64);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -262,8 +292,8 @@ __global__ void __launch_bounds__(384, 1)
   if (pair >= p.pairs) return;
 
   double2* stage0 = sStage + (size_t)pair * 2 * kStageUnits;
-  const uint64_t goff = p.piece_goff[pt];
-  const int sstart = p.piece_start[pt];
+  const uint64_t goff = sGoff[pt];
+  const int sstart = sStart[pt];
   const int rot = pt & 15;
   const uint64_t nb = p.n_blocks;
   const uint64_t npairs = (uint64_t)gridDim.x * p.pairs;
@@ -273,34 +303,49 @@ __global__ void __launch_bounds__(384, 1)
       while (i < nb && i > pair_swap64(i)) i += npairs;
     return i;
   };
-  // where this thread's piece of block i lives: in place, or (packed layout, non-canonical
-  // piece of a block that is not self-transposed) at the transposed position
-  auto piece_src = [&](uint64_t i, bool& tr) {
-    const uint64_t base = insert_zeros10(i, p.lo_mask);
-    const uint64_t e0 = base + goff;
+  // where piece (offset go) of the block at `base` lives: in place, or (packed layout,
+  // non-canonical piece of a block that is not self-transposed) at the transposed position
+  auto piece_src = [&](uint64_t base, bool self, uint64_t go, bool& tr) {
+    const uint64_t e0 = base + go;
     const uint64_t em = pair_swap64(e0);
-    tr = mirror && pair_swap64(base) != base && e0 > em;
+    tr = mirror && !self && e0 > em;
     return tr ? em : e0;
   };
-  auto issue = [&](uint64_t i, int s, bool& tr) {
-    const uint64_t src = piece_src(i, tr);
+  auto is_self = [&](uint64_t base) { return mirror && pair_swap64(base) == base; };
+  auto issue = [&](uint64_t i, int s) {
     uint64_t* bar = &mbar[pair * 2 + s];
+    double2* st = stage0 + s * kStageUnits;
     if (p.dbg & 2) {
-      mbar_arrive_tx(bar, 0);
-    } else {
+      mbar_arrive(bar);
+      return;
+    }
+    const uint64_t base = insert_zeros10(i, p.lo_mask);
+    const bool self = is_self(base);
+    if constexpr (COPY == 0) {
+      bool tr;
+      const uint64_t src = piece_src(base, self, goff, tr);
       mbar_arrive_tx(bar, 256);
-      bulk_g2s(stage0 + s * kStageUnits + sstart, a + src, 256, bar);
+      bulk_g2s(st + sstart, a + src, 256, bar);
+    } else {
+      const int u = pt & 15, qb = pt >> 4;
+#pragma unroll 4
+      for (int it = 0; it < 16; ++it) {
+        const int q = it * 4 + qb;
+        bool tr;
+        const uint64_t src = piece_src(base, self, sGoff[q], tr);
+        cp_async16_cg(st + sStart[q] + u, a + src + u);
+      }
+      cp_async_mbar_arrive(bar);
     }
   };
 
   // this pair's blocks b0, b1, ...: b_k is computed in iteration k from stage k % 2; stages
   // start with b0 and b1; from iteration 1 on, iteration k refills the stage stored in
-  // iteration k-1 with b_{k+1} (after the copy engine has read the stored pieces out)
+  // iteration k-1 with b_{k+1}
   uint64_t cur = next_block((uint64_t)blockIdx.x * p.pairs + pair);
   uint64_t nxt = cur < nb ? next_block(cur + npairs) : nb;
-  bool tr[2] = {false, false};
-  if (cur < nb) issue(cur, 0, tr[0]);
-  if (nxt < nb) issue(nxt, 1, tr[1]);
+  if (cur < nb) issue(cur, 0);
+  if (nxt < nb) issue(nxt, 1);
   uint32_t parity[2] = {0u, 0u};
   bool first = true;
   int s = 0;
@@ -308,9 +353,17 @@ __global__ void __launch_bounds__(384, 1)
     double2* X = stage0 + s * kStageUnits;
     mbar_wait(&mbar[pair * 2 + s], parity[s]);
     parity[s] ^= 1u;
+    if constexpr (COPY == 0) {
+      if (!first) {  // refill the other stage (its bulk stores have read it out)
+        bulk_wait_read0();
+        if (nxt < nb) issue(nxt, s ^ 1);
+      }
+    }
     const uint64_t base = insert_zeros10(cur, p.lo_mask);
-    const bool self = mirror && pair_swap64(base) == base;
-    if (tr[s]) piece_transpose(X + sstart, rot);
+    const bool self = is_self(base);
+    bool trp;
+    piece_src(base, self, goff, trp);  // this thread's piece came from the transpose?
+    if (trp) piece_transpose(X + sstart, rot);
     if (self) {  // non-canonical element <- conj(its transpose, canonical, same block)
       for (int k = 0; k < 16; ++k) {
         const int idx = pt * 16 + ((k + pt) & 15);
@@ -322,46 +375,59 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     pair_bar(pair);
-    if (!first) {  // refill the other stage (stored last iteration) with the next block
-      bulk_wait_read0();
-      if (nxt < nb) issue(nxt, s ^ 1, tr[s ^ 1]);
+    if constexpr (COPY == 1) {
+      // the other stage was read out (LDS) by every pair thread before the barrier above
+      if (!first && nxt < nb) issue(nxt, s ^ 1);
     }
     if (!(p.dbg & 1)) {
+      const bool shared_tab = p.half_add >= 0;
+      double2* Xh = X + (shared_tab ? half * p.half_add : 0);
+      const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
-        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off +
-                            (half * 32 + lane) * (g.k == 2 ? 32 : 16);
+        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(X, F, T, lane);
+          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
         else
-          blk_sub_k1(X, F, T);
+          blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
       }
     }
     pair_bar(pair);
-    if (tr[s]) piece_transpose(X + sstart, rot);
-    fence_async_smem();
+    if (trp) piece_transpose(X + sstart, rot);
+    if constexpr (COPY == 0) fence_async_smem();
     pair_bar(pair);
     if (!(p.dbg & 2)) {
-      bool t2;
-      const uint64_t dst = piece_src(cur, t2);
-      bulk_s2g(a + dst, X + sstart, 256);
-      bulk_commit();
+      if constexpr (COPY == 0) {
+        bool t2;
+        const uint64_t dst = piece_src(base, self, goff, t2);
+        bulk_s2g(a + dst, X + sstart, 256);
+        bulk_commit();
+      } else {
+        const int u = pt & 15, qb = pt >> 4;
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int q = it * 4 + qb;
+          bool tr;
+          const uint64_t dst = piece_src(base, self, sGoff[q], tr);
+          a[dst + u] = X[sStart[q] + u];
+        }
+      }
     }
     first = false;
     cur = nxt;
     nxt = cur < nb ? next_block(cur + npairs) : nb;
     s ^= 1;
   }
-  bulk_wait0();
+  if constexpr (COPY == 0) bulk_wait0();
 }
 
-template <int UI>
+template <int UI, int COPY>
 static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t smem,
                                     cudaStream_t st) {
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = block_kernel<UI>;
+  auto kern = block_kernel<UI, COPY>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -383,13 +449,19 @@ static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t sme
 }
 
 size_t block_smem_bytes(int pairs, int blob_bytes) {
-  return 16 * kBlockMaxPairs + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
+  return kBlockHdrBytes + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
 }
 
+// env TANQ_BLOCK_COPY = bulk | ldg (default): how the block moves between HBM and shared
 cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st) {
+  static int copy = -1;
+  if (copy < 0) {
+    const char* e = getenv("TANQ_BLOCK_COPY");
+    copy = (e && e[0] == 'b') ? 0 : 1;
+  }
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
-  return launch_block_cfg<2>(a, p, smem, st);
+  return copy == 0 ? launch_block_cfg<2, 0>(a, p, smem, st) : launch_block_cfg<2, 1>(a, p, smem, st);
 }
 
 }  // namespace tanq

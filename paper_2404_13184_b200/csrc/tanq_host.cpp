@@ -1323,6 +1323,9 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   }
   p.dbg = (uint32_t)dbg;
   p.n_sub = (int)subs.size();
+  // the warp-half bit is in-piece bit 3 (both halves' offsets differ by 8 units): one table
+  const int halves = half == 3 ? 1 : 2;
+  p.half_add = half == 3 ? 8 : -1;
   // blob: per sub-op fragments then tables (both 16 B aligned)
   size_t off = 0;
   for (size_t i = 0; i < subs.size(); ++i) {
@@ -1367,7 +1370,7 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
           for (int lane = 0; lane < 32; ++lane) {
             const int row = mt * 8 + (lane >> 2), colk = ks * 4 + (lane & 3);
             const double2 v = Sm[(size_t)sub_member(out_bits, 4, row) * 16 + sub_member(in_bits, 4, colk)];
-            const int e = (mt * 4 + ks) * 32 + lane;
+            const int e = (ks * 32 + lane) * 2 + mt;  // [mat][ks][lane][mt]
             F[0 * 256 + e] = v.x;
             F[1 * 256 + e] = -(v.x + v.y);
             F[2 * 256 + e] = v.y - v.x;
@@ -1375,9 +1378,11 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       off += 768 * 8;
       g.t_off = (int)(off / 2);
       T = reinterpret_cast<uint16_t*>(blob + off);
-      for (int h = 0; h < 2; ++h)
+      // layout [4 chunks][rows = halves x 32][8 uint16]: entry e of a row is in chunk e / 8
+      const int rows = halves * 32;
+      for (int h = 0; h < halves; ++h)
         for (int lane = 0; lane < 32; ++lane) {
-          uint16_t* t = T + (h * 32 + lane) * 32;
+          uint16_t t[32];
           const int c4 = lane & 3, r4 = lane >> 2, hb = h << half;
           for (int ks = 0; ks < 4; ++ks)
             for (int j = 0; j < 4; ++j) {
@@ -1392,8 +1397,9 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
                                 deposit(cols.data(), (int)cols.size(), 8 * j + 2 * c4 + c) | hb;
                 t[16 + (mt * 4 + j) * 2 + c] = (uint16_t)slot(idx);
               }
+          for (int e = 0; e < 32; ++e) T[((e >> 3) * rows + h * 32 + lane) * 8 + (e & 7)] = t[e];
         }
-      off += 2 * 32 * 32 * 2;
+      off += (size_t)halves * 32 * 32 * 2;
     } else {
       double2* F = reinterpret_cast<double2*>(blob + off);
       for (int e = 0; e < 16; ++e) F[e] = Sm[e];
@@ -1401,17 +1407,19 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       g.t_off = (int)(off / 2);
       T = reinterpret_cast<uint16_t*>(blob + off);
       const int mbits[2] = {smem_bits[i][0], smem_bits[i][1]};  // member order = sorted position
-      for (int h = 0; h < 2; ++h)
+      const int rows = halves * 32;  // layout [2 chunks][rows][8 uint16]
+      for (int h = 0; h < halves; ++h)
         for (int lane = 0; lane < 32; ++lane) {
-          uint16_t* t = T + (h * 32 + lane) * 16;
+          uint16_t t[16];
           for (int j = 0; j < 4; ++j)
             for (int m = 0; m < 4; ++m) {
               const int idx = deposit(mbits, 2, m) |
                               deposit(cols.data(), (int)cols.size(), lane + 32 * j) | (h << half);
               t[j * 4 + m] = (uint16_t)slot(idx);
             }
+          for (int e = 0; e < 16; ++e) T[((e >> 3) * rows + h * 32 + lane) * 8 + (e & 7)] = t[e];
         }
-      off += 2 * 32 * 16 * 2;
+      off += (size_t)halves * 32 * 16 * 2;
     }
   }
   p.blob_bytes = (int)off;

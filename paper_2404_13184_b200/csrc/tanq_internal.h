@@ -55,8 +55,9 @@ static constexpr int kBlockMaxPairs = 6;
 static constexpr int kBlockMaxSub = 12;
 struct BlockSub {
   int32_t k;       // 1 or 2
-  int32_t a_off;   // doubles: k=2 fragments [3][2][4][32] (a, -(a+b), b-a); k=1: 16 double2
-  int32_t t_off;   // uint16: per-lane shared-memory offset tables [2 halves][32 lanes][32|16]
+  int32_t a_off;   // doubles: k=2 fragments [3][4 ks][32 lanes][2 mt] (a, -(a+b), b-a);
+                   // k=1: 16 double2
+  int32_t t_off;   // uint16: per-lane shared-memory offset tables [1|2 halves][32][32|16]
 };
 struct BlockParams {
   const void* blob;          // sub-op fragments + offset tables (device), copied to shared
@@ -65,7 +66,8 @@ struct BlockParams {
   int32_t pairs;             // warp pairs per CTA (smem-limited, <= kBlockMaxPairs)
   uint32_t mirror;           // packed Hermitian layout
   uint32_t dbg;              // experiments only: 1 skip sub-ops, 2 skip HBM copies
-  uint32_t pad_;
+  int32_t half_add;          // >= 0: one offset table for both warp halves, the second half
+                             // adding half_add units; -1: a table per half
   uint64_t n_blocks;         // 2^(L - 10)
   uint64_t lo_mask[10];      // (1 << pos) - 1 of the 10 block positions, ascending
   uint64_t piece_goff[64];   // element offset of the piece handled by pair thread j

@@ -85,7 +85,7 @@ class tanq_block_params(ctypes.Structure):
     """Mirror of tanq::BlockParams (csrc/tanq_internal.h) for tanq_plan_block_program."""
     _fields_ = [("blob", ctypes.c_void_p), ("blob_bytes", ctypes.c_int32),
                 ("n_sub", ctypes.c_int32), ("pairs", ctypes.c_int32), ("mirror", ctypes.c_uint32),
-                ("dbg", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("dbg", ctypes.c_uint32), ("half_add", ctypes.c_int32),
                 ("n_blocks", ctypes.c_uint64), ("lo_mask", ctypes.c_uint64 * 10),
                 ("piece_goff", ctypes.c_uint64 * 64), ("piece_start", ctypes.c_uint16 * 64),
                 ("start_by_pidx", ctypes.c_uint16 * 64), ("sub", tanq_block_sub * 12)]

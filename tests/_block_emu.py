@@ -38,6 +38,12 @@ def phys_of_rho(rho: np.ndarray, n: int) -> np.ndarray:
     return a, P_r, P_c
 
 
+def lane_table(u16, t_off, rows, row, n):
+    """the n offsets of table row `row` (layout [n / 8 chunks][rows][8 uint16])."""
+    return np.array([u16[t_off + ((e >> 3) * rows + row) * 8 + (e & 7)] for e in range(n)],
+                    dtype=np.int64)
+
+
 def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
     """Run the block program on the physical-order state a (in place)."""
     lo = [int(x) for x in prm.lo_mask]
@@ -74,8 +80,12 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
         for q in range(int(prm.n_sub)):
             g = prm.sub[q]
             for h in range(2):
+                shared = prm.half_add >= 0
+                row0 = 0 if shared else h * 32             # table row of lane 0
+                rows = 32 if shared else 64
+                add = h * prm.half_add if shared else 0    # slot offset of this half
                 if g.k == 2:
-                    F = dbl[g.a_off:g.a_off + 768].reshape(3, 2, 4, 32)
+                    F = dbl[g.a_off:g.a_off + 768].reshape(3, 4, 32, 2).transpose(0, 3, 1, 2)
                     a_ = F[0]
                     b_ = F[2] + F[0]
                     if check:
@@ -84,7 +94,7 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                     X = np.zeros((16, 32), dtype=np.complex128)
                     rd, wr = [], []
                     for lane in range(32):
-                        T = u16[g.t_off + (h * 32 + lane) * 32: g.t_off + (h * 32 + lane + 1) * 32]
+                        T = add + lane_table(u16, g.t_off, rows, row0 + lane, 32)
                         c4, r4 = lane & 3, lane >> 2
                         for mt in range(2):
                             for ks in range(4):
@@ -95,7 +105,7 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                                 rd.append(int(T[ks * 4 + j]))
                     Y = S @ X
                     for lane in range(32):
-                        T = u16[g.t_off + (h * 32 + lane) * 32: g.t_off + (h * 32 + lane + 1) * 32]
+                        T = add + lane_table(u16, g.t_off, rows, row0 + lane, 32)
                         c4, r4 = lane & 3, lane >> 2
                         for mt in range(2):
                             for j in range(4):
@@ -109,7 +119,7 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                     S = (dbl[g.a_off:g.a_off + 32].reshape(16, 2) @ np.array([1, 1j])).reshape(4, 4)
                     rd = []
                     for lane in range(32):
-                        T = u16[g.t_off + (h * 32 + lane) * 16: g.t_off + (h * 32 + lane + 1) * 16]
+                        T = add + lane_table(u16, g.t_off, rows, row0 + lane, 16)
                         for j in range(4):
                             offs = [int(T[j * 4 + m]) for m in range(4)]
                             rd += offs

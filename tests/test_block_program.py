@@ -12,7 +12,7 @@ import pytest
 import workloads as W
 from oracle import dense
 
-from _block_emu import emulate, pair_swap, phys_of_rho
+from _block_emu import emulate, lane_table, pair_swap, phys_of_rho
 
 
 @pytest.fixture(scope="module")
@@ -75,8 +75,9 @@ def _bank_degrees(prm, blob):
         g = prm.sub[q]
         if g.k != 2:
             continue
-        for h in range(2):
-            T = np.array([u16[g.t_off + (h * 32 + l) * 32: g.t_off + (h * 32 + l + 1) * 32]
+        rows = 32 if prm.half_add >= 0 else 64
+        for h in range(rows // 32):
+            T = np.array([lane_table(u16, g.t_off, rows, h * 32 + l, 32)
                           for l in range(32)])               # [lane][32]
             for e in range(32):
                 for ph in range(4):

@@ -32,6 +32,7 @@
 // precomputed fragments, so the only FP64 adds left are the c+d of each B element.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <atomic>
@@ -126,25 +127,31 @@ __device__ __forceinline__ uint64_t insert_zeros10(uint64_t t, const uint64_t* l
 // 16-element piece, in-piece index t = (r0 c0 r1 c1): transpose swaps each row/col bit pair.
 __device__ __forceinline__ int pswap4(int t) { return ((t & 5) << 1) | ((t >> 1) & 5); }
 
-// In-place (permute + conjugate) of one piece: X[pswap4(t)] <- conj(X[t]).  Involution.  The
-// start offset `rot` spreads the lanes of a warp over the banks.
+// In-place (permute + conjugate) of one piece: X[pswap4(t)] <- conj(X[t]).  Involution.  Lane
+// j of a quarter warp visits t = i ^ rot(j), rot = {0,1,2,3,12,13,14,15}[j]: both t and
+// pswap4(t) = pswap4(i) ^ pswap4(rot) then cover all 8 banks, so loads and stores are
+// conflict-free (for pieces with the same bank rotation).
+__device__ __forceinline__ int piece_rot(int j) { return (j & 4) ? 8 + j : j & 3; }
 __device__ __forceinline__ void piece_transpose(double2* P, int rot) {
   double2 v[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = P[(i + rot) & 15];
+  for (int i = 0; i < 16; ++i) v[i] = P[i ^ rot];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) P[pswap4((i + rot) & 15)] = make_double2(v[i].x, -v[i].y);
+  for (int i = 0; i < 16; ++i) P[pswap4(i ^ rot)] = make_double2(v[i].x, -v[i].y);
 }
 
 // k = 2 sub-op on one warp's half block.  F: fragments [3][4 ks][32 lanes][2 mt] doubles
 // (a, -(a+b), b-a); T: this lane's 32 offsets (16 B-fragment [ks][j], 16 D-fragment [mt][j][c]).
 template <int UI>
 __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const uint16_t* T,
-                                           int lane, int trow, int rows) {
+                                           int lane, int trow, int rows, uint32_t tm) {
+  // tm: nonzero 8x4 tiles of S (bit mt * 4 + ks); zero tiles issue no DMMA, k-steps whose two
+  // tiles are both zero load no B fragment.  Warp-uniform.
   double a1[2][4], a2[2][4], a3[2][4];
   const double2* F2 = reinterpret_cast<const double2*>(F);  // [mat][ks][lane] = (mt 0, mt 1)
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
+    if (!((tm >> ks) & 0x11u)) continue;
     const double2 v1 = F2[(0 * 4 + ks) * 32 + lane], v2 = F2[(1 * 4 + ks) * 32 + lane],
                   v3 = F2[(2 * 4 + ks) * 32 + lane];
     a1[0][ks] = v1.x; a1[1][ks] = v1.y;
@@ -173,39 +180,43 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
   for (int n0 = 0; n0 < 4; n0 += UI) {
     double2 xb[UI][4];
 #pragma unroll
-    for (int u = 0; u < UI; ++u)
+    for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) xb[u][ks] = X[boff(ks, n0 + u)];
+      for (int u = 0; u < UI; ++u)
+        xb[u][ks] = ((tm >> ks) & 0x11u) ? X[boff(ks, n0 + u)] : make_double2(0.0, 0.0);
     double k1[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) k1[u][mt][0] = k1[u][mt][1] = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
+    for (int ks = 0; ks < 4; ++ks) {
+      if (!((tm >> ks) & 0x11u)) continue;
 #pragma unroll
       for (int u = 0; u < UI; ++u) {
-        const double s = xb[u][ks].x + xb[u][ks].y;
+        const double sx = xb[u][ks].x + xb[u][ks].y;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], s);
+        for (int mt = 0; mt < 2; ++mt)
+          if ((tm >> (mt * 4 + ks)) & 1u) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], sx);
       }
+    }
     double yr[UI][2][2], yi[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb[u][0].y, k1[u][mt][0], k1[u][mt][1]);
-        dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb[u][0].x, k1[u][mt][0], k1[u][mt][1]);
-      }
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int ks = 1; ks < 4; ++ks)
+        for (int c = 0; c < 2; ++c) yr[u][mt][c] = yi[u][mt][c] = k1[u][mt][c];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
       for (int u = 0; u < UI; ++u)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
-          dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
-        }
+        for (int mt = 0; mt < 2; ++mt)
+          if ((tm >> (mt * 4 + ks)) & 1u) {
+            dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
+            dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+          }
     __syncwarp();  // every lane's B loads of this pass precede any lane's D stores
 #pragma unroll
     for (int u = 0; u < UI; ++u)
@@ -257,7 +268,9 @@ __device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const ui
 
 constexpr int kStageUnits = 1032;  // 16 x 64 + rotation slack (<= 7), rounded to 8 units
 // shared header: mbarriers [2 * kBlockMaxPairs], piece offsets [64] (u64), starts [64] (u16)
-constexpr int kBlockHdrBytes = 768;
+constexpr int kBlockHdrBytes = 896;
+constexpr int kBlockHdrBytesWs = 896;  // full + done mbarriers, piece tables
+static_assert(32 * kBlockMaxPairs + 64 * 8 + 64 * 2 <= kBlockHdrBytesWs, "block header (ws)");
 static_assert(16 * kBlockMaxPairs + 64 * 8 + 64 * 2 <= kBlockHdrBytes, "block header");
 
 // COPY = 0: every pair thread moves one 256 B piece with cp.async.bulk (G2S with mbarrier
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(384, 1)
   double2* stage0 = sStage + (size_t)pair * 2 * kStageUnits;
   const uint64_t goff = sGoff[pt];
   const int sstart = sStart[pt];
-  const int rot = pt & 15;
+  const int rot = piece_rot(pt & 7);
   const uint64_t nb = p.n_blocks;
   const uint64_t npairs = (uint64_t)gridDim.x * p.pairs;
   const bool mirror = p.mirror != 0;
@@ -388,7 +401,7 @@ __global__ void __launch_bounds__(384, 1)
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
+          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows, (uint32_t)g.tmask);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
@@ -423,6 +436,178 @@ __global__ void __launch_bounds__(384, 1)
   if constexpr (COPY == 0) bulk_wait0();
 }
 
+// Warp-specialised variant (COPY = 2): 2 producer warps (the last two of the CTA) move every
+// block of 3 pairs each -- bulk G2S loads onto `full` mbarriers (arrive.expect_tx 16 KB) and bulk
+// S2G stores once the pair's 64 consumer threads have arrived on `done` -- so the consumer
+// warps run only fixups and the sub-op DMMA program.  A stage is refilled with the pair's block
+// k + 2 as soon as the bulk stores of block k have read it out (cp.async.bulk.wait_group.read).
+template <int UI>
+__global__ void __launch_bounds__(448)
+    block_kernel_ws(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);  // full [2P] | done [2P]
+  uint64_t* sGoff = mbar + 4 * kBlockMaxPairs;
+  uint16_t* sStart = reinterpret_cast<uint16_t*>(sGoff + 64);
+  unsigned char* sBlob = smem_raw + kBlockHdrBytesWs;
+  double2* sStage = reinterpret_cast<double2*>(sBlob + p.blob_bytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = p.pairs;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.blob);
+    uint4* dst = reinterpret_cast<uint4*>(sBlob);
+    for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x < 64) {
+      sGoff[threadIdx.x] = p.piece_goff[threadIdx.x];
+      sStart[threadIdx.x] = p.piece_start[threadIdx.x];
+    }
+    if (threadIdx.x < 2 * P) {
+      mbar_init(&mbar[threadIdx.x], 1);                   // full: the producer's expect_tx
+      mbar_init(&mbar[2 * kBlockMaxPairs + threadIdx.x], 64);  // done: the pair's threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t nb = p.n_blocks;
+  const uint64_t npairs = (uint64_t)gridDim.x * P;
+  const bool mirror = p.mirror != 0;
+  auto next_block = [&](uint64_t i) {
+    if (mirror)
+      while (i < nb && i > pair_swap64(i)) i += npairs;
+    return i;
+  };
+  auto is_self = [&](uint64_t base) { return mirror && pair_swap64(base) == base; };
+  auto piece_src = [&](uint64_t base, bool self, uint64_t go, bool& tr) {
+    const uint64_t e0 = base + go;
+    const uint64_t em = pair_swap64(e0);
+    tr = mirror && !self && e0 > em;
+    return tr ? em : e0;
+  };
+  uint64_t* full = mbar;
+  uint64_t* done = mbar + 2 * kBlockMaxPairs;
+
+  if (warp >= 2 * P) {
+    // ------------------------------ producers ------------------------------
+    const int w = warp - 2 * P;  // 0 or 1: pairs w, w + 2, w + 4
+    auto load = [&](int pr, int st, uint64_t i) {
+      uint64_t* bar = &full[pr * 2 + st];
+      if (lane == 0) mbar_arrive_tx(bar, (p.dbg & 2) ? 0u : 16384u);
+      if (p.dbg & 2) return;
+      __syncwarp();
+      const uint64_t base = insert_zeros10(i, p.lo_mask);
+      const bool self = is_self(base);
+      double2* stg = sStage + ((size_t)pr * 2 + st) * kStageUnits;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = lane + 32 * h;
+        bool tr;
+        const uint64_t src = piece_src(base, self, sGoff[r], tr);
+        bulk_g2s(stg + sStart[r], a + src, 256, bar);
+      }
+    };
+    auto store = [&](int pr, int st, uint64_t i) {
+      if (p.dbg & 2) return;
+      const uint64_t base = insert_zeros10(i, p.lo_mask);
+      const bool self = is_self(base);
+      const double2* stg = sStage + ((size_t)pr * 2 + st) * kStageUnits;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = lane + 32 * h;
+        bool tr;
+        const uint64_t dst = piece_src(base, self, sGoff[r], tr);
+        bulk_s2g(a + dst, stg + sStart[r], 256);
+      }
+      bulk_commit();
+    };
+    uint64_t bk[3], b1[3], bk2[3];  // per served pair: blocks of iterations k, k+1, k+2
+    int prs[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      prs[j] = w + 2 * j;
+      const bool ok = prs[j] < P;
+      bk[j] = ok ? next_block((uint64_t)blockIdx.x * P + prs[j]) : nb;
+      b1[j] = bk[j] < nb ? next_block(bk[j] + npairs) : nb;
+      if (bk[j] < nb) load(prs[j], 0, bk[j]);
+      if (b1[j] < nb) load(prs[j], 1, b1[j]);
+      bk2[j] = b1[j] < nb ? next_block(b1[j] + npairs) : nb;
+    }
+    for (uint32_t k = 0;; ++k) {
+      const int st = k & 1;
+      const uint32_t par = (k >> 1) & 1;
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (bk[j] >= nb) continue;
+        any = true;
+        mbar_wait(&done[prs[j] * 2 + st], par);
+        store(prs[j], st, bk[j]);
+      }
+      if (!any) break;
+      bulk_wait_read0();  // the stores above have read their stages out
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (bk[j] >= nb) continue;
+        if (bk2[j] < nb) load(prs[j], st, bk2[j]);
+        // iteration k + 1 handles b_{k+1}; b_{k+3} follows b_{k+2}
+        const uint64_t nk = b1[j];
+        b1[j] = bk2[j];
+        bk2[j] = bk2[j] < nb ? next_block(bk2[j] + npairs) : nb;
+        bk[j] = nk;
+      }
+    }
+    bulk_wait0();
+    return;
+  }
+
+  // ------------------------------ consumers ------------------------------
+  const int pair = warp >> 1, half = warp & 1, pt = threadIdx.x & 63;
+  double2* stage0 = sStage + (size_t)pair * 2 * kStageUnits;
+  const uint64_t goff = sGoff[pt];
+  const int sstart = sStart[pt];
+  const int rot = piece_rot(pt & 7);
+  uint64_t cur = next_block((uint64_t)blockIdx.x * P + pair);
+  for (uint32_t k = 0; cur < nb; ++k) {
+    const int st = k & 1;
+    double2* X = stage0 + st * kStageUnits;
+    mbar_wait(&full[pair * 2 + st], (k >> 1) & 1);
+    const uint64_t base = insert_zeros10(cur, p.lo_mask);
+    const bool self = is_self(base);
+    bool trp;
+    piece_src(base, self, goff, trp);
+    if (trp) piece_transpose(X + sstart, rot);
+    if (self) {
+      for (int kk = 0; kk < 16; ++kk) {
+        const int idx = pt * 16 + ((kk + pt) & 15);
+        const int idm = ((idx & 0x155) << 1) | ((idx >> 1) & 0x155);
+        if (idx > idm) {
+          const double2 v = X[p.start_by_pidx[idm >> 4] + (idm & 15)];
+          X[p.start_by_pidx[idx >> 4] + (idx & 15)] = make_double2(v.x, -v.y);
+        }
+      }
+    }
+    pair_bar(pair);
+    if (!(p.dbg & 1)) {
+      const bool shared_tab = p.half_add >= 0;
+      double2* Xh = X + (shared_tab ? half * p.half_add : 0);
+      const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
+      for (int q = 0; q < p.n_sub; ++q) {
+        const BlockSub& g = p.sub[q];
+        const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
+        if (g.k == 2)
+          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows, (uint32_t)g.tmask);
+        else
+          blk_sub_k1(Xh, F, T, trow, trows);
+        __syncwarp();
+      }
+    }
+    pair_bar(pair);
+    if (trp) piece_transpose(X + sstart, rot);
+    fence_async_smem();
+    mbar_arrive(&done[pair * 2 + st]);
+    cur = next_block(cur + npairs);
+  }
+}
+
 template <int UI, int COPY>
 static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t smem,
                                     cudaStream_t st) {
@@ -452,15 +637,51 @@ size_t block_smem_bytes(int pairs, int blob_bytes) {
   return kBlockHdrBytes + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
 }
 
-// env TANQ_BLOCK_COPY = bulk | ldg (default): how the block moves between HBM and shared
+// env TANQ_BLOCK_COPY = ws (default: warp-specialised producers) | bulk | ldg: how blocks move
+// between HBM and shared memory
 cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st) {
   static int copy = -1;
   if (copy < 0) {
     const char* e = getenv("TANQ_BLOCK_COPY");
-    copy = (e && e[0] == 'b') ? 0 : 1;
+    copy = !e ? 2 : (e[0] == 'b' ? 0 : (e[0] == 'l' ? 1 : 2));
   }
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
+  if (copy == 2) {
+    static std::atomic<uint64_t> attr_done{0};
+    auto kern = block_kernel_ws<2>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = (uint64_t)1 << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr_done.fetch_or(bit);
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (p.n_blocks + p.pairs - 1) / p.pairs;
+    unsigned grid = (unsigned)(want < (uint64_t)sms ? want : (uint64_t)sms);
+    const char* cap = getenv("TANQ_GRID_CAP");
+    if (cap && atoi(cap) > 0 && grid > (unsigned)atoi(cap)) grid = (unsigned)atoi(cap);
+    if (grid < 1) grid = 1;
+    kern<<<grid, 64 * p.pairs + 64, smem, st>>>(a, p);
+    e = cudaGetLastError();
+    if (e == cudaErrorLaunchOutOfResources) {  // diagnostics for the error message
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
+        char msg[256];
+        snprintf(msg, sizeof msg,
+                 "block_kernel_ws: %d threads, %zu B dynamic smem; kernel: %d regs, max %d "
+                 "threads, %zu B static smem, %zu B local",
+                 64 * p.pairs + 64, smem, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+                 fa.localSizeBytes);
+        set_error(msg);
+      }
+    }
+    return e;
+  }
   return copy == 0 ? launch_block_cfg<2, 0>(a, p, smem, st) : launch_block_cfg<2, 1>(a, p, smem, st);
 }
 

@@ -1178,12 +1178,31 @@ int phase_degree(int w0, int w1, int w2) {  // max lanes per bank over the 8 com
 }
 
 struct BlockSubChoice {
-  int k0 = 0, k1 = 0, o0 = 0, n[3] = {0, 0, 0}, cost = 0;
+  int k0 = 0, k1 = 0, o0 = 0, o3 = 0, n[3] = {0, 0, 0}, cost = 0, tiles = 8;
+  uint32_t tmask = 0xffu;  // nonzero 8x4 A tiles (bit mt * 4 + ks)
 };
 
-// best lane mapping of one sub-op (member / column block bits) for bank weights w
+// nonzero 8x4 A tiles of a k=2 sub-op (16x16, sub-op member order, nz[out * 16 + in]) when
+// in-index bits (0, 1) = members (i, j), ks = the other two (ascending), and mt = member o3
+uint32_t tile_mask(const uint8_t* nz, int i, int j, int o3) {
+  int kb[2], nk = 0;
+  for (int t = 0; t < 4; ++t)
+    if (t != i && t != j) kb[nk++] = t;
+  uint32_t m = 0;
+  for (int mo = 0; mo < 16; ++mo)
+    for (int mi = 0; mi < 16; ++mi)
+      if (nz[mo * 16 + mi]) {
+        const int mt = (mo >> o3) & 1, ks = ((mi >> kb[0]) & 1) | (((mi >> kb[1]) & 1) << 1);
+        m |= 1u << (mt * 4 + ks);
+      }
+  return m;
+}
+
+// best lane mapping of one sub-op (member / column block bits) for bank weights w.  k = 2:
+// fewest nonzero A tiles first (every zero 8x4 tile saves 3 DMMA per n-tile pass), then the
+// fewest bank conflicts of the B (k0, k1, n0) and D (o0, n1, n2) quarter-warp accesses.
 BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector<int>& col,
-                           const int* w) {
+                           const int* w, const uint8_t* nz = nullptr) {
   BlockSubChoice best;
   best.cost = 1 << 20;
   if (k == 1) {  // lanes vary column bits n0..n2 (col = lane + 32 j)
@@ -1201,25 +1220,40 @@ BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector
         }
     return best;
   }
+  int dB[4][4][8], dD[4][8][8];  // bank degrees by (i, j, a) and (o, b, c)
+  const int nc = (int)col.size();
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      for (int a = 0; a < nc; ++a) dB[i][j][a] = phase_degree(w[mem[i]], w[mem[j]], w[col[a]]);
+  for (int o = 0; o < 4; ++o)
+    for (int b = 0; b < nc; ++b)
+      for (int c = 0; c < nc; ++c) dD[o][b][c] = phase_degree(w[mem[o]], w[col[b]], w[col[c]]);
   for (int i = 0; i < 4; ++i)
     for (int j = i + 1; j < 4; ++j)
-      for (size_t a = 0; a < col.size(); ++a) {
-        const int db = phase_degree(w[mem[i]], w[mem[j]], w[col[a]]);
-        for (int o = 0; o < 4; ++o)
-          for (size_t b = 0; b < col.size(); ++b)
-            for (size_t c = b + 1; c < col.size(); ++c) {
-              if (b == a || c == a) continue;
-              const int dd = phase_degree(w[mem[o]], w[col[b]], w[col[c]]);
-              if (db + dd < best.cost) {
-                best.cost = db + dd;
-                best.k0 = mem[i];
-                best.k1 = mem[j];
-                best.o0 = mem[o];
-                best.n[0] = col[a];
-                best.n[1] = col[b];
-                best.n[2] = col[c];
+      for (int o3 = 0; o3 < 4; ++o3) {
+        const uint32_t tm = nz ? tile_mask(nz, i, j, o3) : 0xffu;
+        const int tiles = __builtin_popcount(tm);
+        for (int o = 0; o < 4; ++o) {
+          if (o == o3) continue;
+          for (int a = 0; a < nc; ++a)
+            for (int b = 0; b < nc; ++b)
+              for (int c = b + 1; c < nc; ++c) {
+                if (b == a || c == a) continue;
+                const int cost = 100 * tiles + dB[i][j][a] + dD[o][b][c];
+                if (cost < best.cost) {
+                  best.cost = cost;
+                  best.tiles = tiles;
+                  best.tmask = tm;
+                  best.k0 = mem[i];
+                  best.k1 = mem[j];
+                  best.o0 = mem[o];
+                  best.o3 = mem[o3];
+                  best.n[0] = col[a];
+                  best.n[1] = col[b];
+                  best.n[2] = col[c];
+                }
               }
-            }
+        }
       }
   return best;
 }
@@ -1249,8 +1283,14 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   // member / column block bits of every sub-op
   std::vector<std::vector<int>> smem_bits(subs.size()), scol_bits(subs.size());
   std::vector<MemberMap> smap(subs.size());
+  std::vector<std::vector<uint8_t>> snz(subs.size());  // nonzero pattern, sub-op member order
   for (size_t i = 0; i < subs.size(); ++i) {
     smap[i] = member_map(s, subs[i]->k, subs[i]->q);
+    if (subs[i]->k == 2) {
+      const std::vector<double2> Sm = member_order_S(*subs[i], smap[i]);
+      snz[i].resize(256);
+      for (int e = 0; e < 256; ++e) snz[i][e] = (Sm[e].x != 0.0 || Sm[e].y != 0.0) ? 1 : 0;
+    }
     for (int t = 0; t < 2 * subs[i]->k; ++t) smem_bits[i].push_back(bit_of_pos(smap[i].bits[t].first));
     for (int j = 0; j < 10; ++j)
       if (j != half && std::find(smem_bits[i].begin(), smem_bits[i].end(), j) == smem_bits[i].end())
@@ -1273,13 +1313,25 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   auto total_cost = [&](const int* ww) {
     int c = 0;
     for (size_t i = 0; i < subs.size(); ++i)
-      c += best_choice(subs[i]->k, smem_bits[i], scol_bits[i], ww).cost;
+      c += best_choice(subs[i]->k, smem_bits[i], scol_bits[i], ww,
+                       snz[i].empty() ? nullptr : snz[i].data()).cost;
     return c;
   };
   int cost = total_cost(w);
-  const int ideal = [&] {
+  const int ideal = [&] {  // every sub-op at its fewest tiles and conflict-free
     int c = 0;
-    for (const auto* sb : subs) c += sb->k == 2 ? 2 : 1;
+    for (size_t i = 0; i < subs.size(); ++i) {
+      if (subs[i]->k != 2) {
+        c += 1;
+        continue;
+      }
+      int tmin = 8;
+      for (int a = 0; a < 4; ++a)
+        for (int b = a + 1; b < 4; ++b)
+          for (int o3 = 0; o3 < 4; ++o3)
+            tmin = std::min(tmin, __builtin_popcount(tile_mask(snz[i].data(), a, b, o3)));
+      c += 100 * tmin + 2;
+    }
     return c;
   }();
   for (int sweep = 0; sweep < 4 && cost > ideal; ++sweep)
@@ -1332,7 +1384,9 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     const FusedOp& sb = *subs[i];
     tanq::BlockSub& g = p.sub[i];
     g.k = sb.k;
-    const BlockSubChoice ch = best_choice(sb.k, smem_bits[i], scol_bits[i], w);
+    const BlockSubChoice ch = best_choice(sb.k, smem_bits[i], scol_bits[i], w,
+                                          snz[i].empty() ? nullptr : snz[i].data());
+    g.tmask = sb.k == 2 ? (int)ch.tmask : 0xff;
     const std::vector<double2> Sm = member_order_S(sb, smap[i]);  // sub-op member order
     // sub-op member bit t <-> block bit smem_bits[i][t]
     auto sub_member = [&](const int* blkbits, int nb, int v) {  // value over blkbits -> member
@@ -1358,11 +1412,11 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     g.a_off = (int)(off / 8);
     uint16_t* T;
     if (sb.k == 2) {
-      int in_bits[4] = {ch.k0, ch.k1, 0, 0}, out_bits[4] = {ch.o0, 0, 0, 0};
+      int in_bits[4] = {ch.k0, ch.k1, 0, 0}, out_bits[4] = {ch.o0, 0, 0, ch.o3};
       for (int t = 0, a = 2, b = 1; t < 4; ++t) {
         const int bb = smem_bits[i][t];
         if (bb != ch.k0 && bb != ch.k1) in_bits[a++] = bb;
-        if (bb != ch.o0) out_bits[b++] = bb;
+        if (bb != ch.o0 && bb != ch.o3) out_bits[b++] = bb;
       }
       double* F = reinterpret_cast<double*>(blob + off);
       for (int mt = 0; mt < 2; ++mt)
@@ -1484,7 +1538,11 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       if (bp) {
         tanq::BlockParams p = *bp;
         p.blob = (*prog)[di];
-        CUDA_TRY(tanq::launch_block_group(sh.data, p, sh.stream));
+        g_err.clear();
+        const cudaError_t be = tanq::launch_block_group(sh.data, p, sh.stream);
+        if (be != cudaSuccess)
+          return fail(TANQ_E_CUDA, std::string("launch_block_group -> ") + cudaGetErrorString(be) +
+                                       (g_err.empty() ? "" : " [" + g_err + "]"));
       } else {
         tanq::GroupParams p = *gp;
         p.prog = (*prog)[di];

@@ -58,6 +58,7 @@ struct BlockSub {
   int32_t a_off;   // doubles: k=2 fragments [3][4 ks][32 lanes][2 mt] (a, -(a+b), b-a);
                    // k=1: 16 double2
   int32_t t_off;   // uint16: per-lane shared-memory offset tables [1|2 halves][32][32|16]
+  int32_t tmask;   // k=2: nonzero 8x4 A tiles, bit mt * 4 + ks (zero tiles are skipped)
 };
 struct BlockParams {
   const void* blob;          // sub-op fragments + offset tables (device), copied to shared

@@ -90,6 +90,10 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                     b_ = F[2] + F[0]
                     if check:
                         assert np.allclose(F[1], -(a_ + b_), atol=1e-14, rtol=1e-14)
+                        for mt in range(2):       # tiles the kernel skips are exactly zero
+                            for ks in range(4):
+                                if not (int(g.tmask) >> (mt * 4 + ks)) & 1:
+                                    assert not F[:, mt, ks, :].any(), (q, mt, ks)
                     S = np.zeros((16, 16), dtype=np.complex128)
                     X = np.zeros((16, 32), dtype=np.complex128)
                     rd, wr = [], []

@@ -144,14 +144,11 @@ __device__ __forceinline__ void piece_transpose(double2* P, int rot) {
 // (a, -(a+b), b-a); T: this lane's 32 offsets (16 B-fragment [ks][j], 16 D-fragment [mt][j][c]).
 template <int UI>
 __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const uint16_t* T,
-                                           int lane, int trow, int rows, uint32_t tm) {
-  // tm: nonzero 8x4 tiles of S (bit mt * 4 + ks); zero tiles issue no DMMA, k-steps whose two
-  // tiles are both zero load no B fragment.  Warp-uniform.
+                                           int lane, int trow, int rows) {
   double a1[2][4], a2[2][4], a3[2][4];
   const double2* F2 = reinterpret_cast<const double2*>(F);  // [mat][ks][lane] = (mt 0, mt 1)
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
-    if (!((tm >> ks) & 0x11u)) continue;
     const double2 v1 = F2[(0 * 4 + ks) * 32 + lane], v2 = F2[(1 * 4 + ks) * 32 + lane],
                   v3 = F2[(2 * 4 + ks) * 32 + lane];
     a1[0][ks] = v1.x; a1[1][ks] = v1.y;
@@ -180,43 +177,39 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
   for (int n0 = 0; n0 < 4; n0 += UI) {
     double2 xb[UI][4];
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
+    for (int u = 0; u < UI; ++u)
 #pragma unroll
-      for (int u = 0; u < UI; ++u)
-        xb[u][ks] = ((tm >> ks) & 0x11u) ? X[boff(ks, n0 + u)] : make_double2(0.0, 0.0);
+      for (int ks = 0; ks < 4; ++ks) xb[u][ks] = X[boff(ks, n0 + u)];
     double k1[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) k1[u][mt][0] = k1[u][mt][1] = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      if (!((tm >> ks) & 0x11u)) continue;
+    for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
       for (int u = 0; u < UI; ++u) {
         const double sx = xb[u][ks].x + xb[u][ks].y;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-          if ((tm >> (mt * 4 + ks)) & 1u) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], sx);
+        for (int mt = 0; mt < 2; ++mt) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], sx);
       }
-    }
     double yr[UI][2][2], yi[UI][2][2];
 #pragma unroll
     for (int u = 0; u < UI; ++u)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb[u][0].y, k1[u][mt][0], k1[u][mt][1]);
+        dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb[u][0].x, k1[u][mt][0], k1[u][mt][1]);
+      }
 #pragma unroll
-        for (int c = 0; c < 2; ++c) yr[u][mt][c] = yi[u][mt][c] = k1[u][mt][c];
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
+    for (int ks = 1; ks < 4; ++ks)
 #pragma unroll
       for (int u = 0; u < UI; ++u)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-          if ((tm >> (mt * 4 + ks)) & 1u) {
-            dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
-            dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
-          }
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
+          dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+        }
     __syncwarp();  // every lane's B loads of this pass precede any lane's D stores
 #pragma unroll
     for (int u = 0; u < UI; ++u)
@@ -401,7 +394,7 @@ __global__ void __launch_bounds__(384, 1)
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows, (uint32_t)g.tmask);
+          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
@@ -594,7 +587,7 @@ __global__ void __launch_bounds__(448)
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows, (uint32_t)g.tmask);
+          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
@@ -637,13 +630,15 @@ size_t block_smem_bytes(int pairs, int blob_bytes) {
   return kBlockHdrBytes + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
 }
 
-// env TANQ_BLOCK_COPY = ws (default: warp-specialised producers) | bulk | ldg: how blocks move
-// between HBM and shared memory
+// env TANQ_BLOCK_COPY = bulk (default) | ws (warp-specialised producers) | ldg: how blocks move
+// between HBM and shared memory.  Measured at n = 16 (profiles/r02_block_copy_variants.txt):
+// bulk 15.5-17.7 ms per 2-sub-op group, ldg 16.7-21.4, ws 33 (2 producer warps cannot issue
+// 256 B bulk copies fast enough: ~65 clock cycles per copy per warp).
 cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st) {
   static int copy = -1;
   if (copy < 0) {
     const char* e = getenv("TANQ_BLOCK_COPY");
-    copy = !e ? 2 : (e[0] == 'b' ? 0 : (e[0] == 'l' ? 1 : 2));
+    copy = !e ? 0 : (e[0] == 'w' ? 2 : (e[0] == 'l' ? 1 : 0));
   }
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;

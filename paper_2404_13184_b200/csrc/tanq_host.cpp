@@ -1156,9 +1156,20 @@ int block_pairs_for(size_t blob_bytes) {
 
 // Ops the block kernel runs: 3-qubit groups of k <= 2 sub-ops (not dense k = 3 ops), at least
 // 4 blocks, small enough programs.  Env TANQ_BLOCK=0 restores the round-1 group kernels.
+bool block_k2_enabled() {  // env TANQ_BLOCK_K2=1: standalone k = 2 ops through the block kernel too
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TANQ_BLOCK_K2");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 bool block_ok(const tanq_sim* s, const FusedOp& op) {
-  if (!block_enabled() || op.k != 3 || op.sub.empty()) return false;
-  if ((int)op.sub.size() > tanq::kBlockMaxSub || s->L < 12) return false;
+  if (!block_enabled() || s->L < 12) return false;
+  if (op.k == 2 && op.sub.empty()) return block_k2_enabled() && k2_tiled(s, op);
+  if (op.k != 3 || op.sub.empty()) return false;
+  if ((int)op.sub.size() > tanq::kBlockMaxSub) return false;
   for (const auto& sb : op.sub)
     if (sb.k > 2) return false;
   return block_pairs_for(block_blob_bytes(op)) > 0;
@@ -1176,6 +1187,11 @@ int phase_degree(int w0, int w1, int w2) {  // max lanes per bank over the 8 com
   }
   return mx;
 }
+
+// Zero-tile skipping (BlockSub::tmask) measured slower on B200 (uniform branches around the
+// DMMAs and +16 registers cost more than the 25% of DMMAs QPE's sparse sub-ops save), so the
+// kernel issues every tile and the mapping is chosen for bank conflicts only (weight 0).
+constexpr int kTileWeight = 0;
 
 struct BlockSubChoice {
   int k0 = 0, k1 = 0, o0 = 0, o3 = 0, n[3] = {0, 0, 0}, cost = 0, tiles = 8;
@@ -1239,7 +1255,7 @@ BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector
             for (int b = 0; b < nc; ++b)
               for (int c = b + 1; c < nc; ++c) {
                 if (b == a || c == a) continue;
-                const int cost = 100 * tiles + dB[i][j][a] + dD[o][b][c];
+                const int cost = kTileWeight * tiles + dB[i][j][a] + dD[o][b][c];
                 if (cost < best.cost) {
                   best.cost = cost;
                   best.tiles = tiles;
@@ -1280,6 +1296,7 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     if (is_member[j] < 0) half = j;
   std::vector<const FusedOp*> subs;
   for (const auto& sb : op.sub) subs.push_back(&sb);
+  if (subs.empty()) subs.push_back(&op);  // a standalone k = 2 op: one sub-op on 2 qubits
   // member / column block bits of every sub-op
   std::vector<std::vector<int>> smem_bits(subs.size()), scol_bits(subs.size());
   std::vector<MemberMap> smap(subs.size());
@@ -1330,7 +1347,7 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
         for (int b = a + 1; b < 4; ++b)
           for (int o3 = 0; o3 < 4; ++o3)
             tmin = std::min(tmin, __builtin_popcount(tile_mask(snz[i].data(), a, b, o3)));
-      c += 100 * tmin + 2;
+      c += kTileWeight * tmin + 2;
     }
     return c;
   }();

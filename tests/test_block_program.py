@@ -101,3 +101,49 @@ def test_block_layout_bank_conflict_free(Plan):
         assert _bank_degrees(*prog) == 1, (i, qs)
         seen += 1
     assert seen >= 3
+
+
+K2_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, %(root)r); sys.path.insert(0, %(tests)r)
+import workloads as W
+from oracle import dense
+from paper_2404_13184_b200.tanq import Plan
+from _block_emu import emulate, pair_swap, phys_of_rho
+n = 7
+rng = np.random.default_rng(3)
+ops = [W.Op("kraus", (5, 6), kraus=W.random_kraus(rng, 4, 2)),
+       W.Op("u", (1, 4), mat=W.random_unitary(rng, 4))]
+plan = Plan(None, W.Circuit(n, ops), None, fuse=0, k_max=2)
+seen = 0
+for i, (qs, S) in enumerate(plan.ops()):
+    for packed in (True, False):
+        prog = plan.block_program(i, packed=packed)
+        if prog is None:
+            continue
+        rho = W.random_density(rng, n, rank=3)
+        a, _, _ = phys_of_rho(rho, n)
+        emulate(a, *prog)
+        ref = np.ascontiguousarray(rho.copy()); dense.apply_superop(ref, n, qs, S)
+        aref, _, _ = phys_of_rho(ref, n)
+        P = np.arange(4 ** n)
+        keep = np.array([p <= pair_swap(int(p)) for p in P]) if packed else np.ones(4 ** n, bool)
+        assert np.abs(a[keep] - aref[keep]).max() < 1e-12
+        seen += 1
+assert seen >= 2, seen
+print("OK", seen)
+"""
+
+
+def test_block_program_standalone_k2():
+    """TANQ_BLOCK_K2=1: standalone k=2 ops with a target at physical position >= 6 run as a
+    one-sub-op block program (2 group qubits + 3 free qubits per block)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, TANQ_BLOCK_K2="1")
+    r = subprocess.run([sys.executable, "-c", K2_SNIPPET % {"root": os.path.dirname(here),
+                                                             "tests": here}],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr

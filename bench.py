@@ -285,7 +285,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
+    if world != args.gpus and args.remap != "p2p":
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     # TANQ_NCCL_LIB = the NCCL test shim (tests/nccl_shim): ranks may share one GPU, the
     # torch-level plumbing runs on gloo; a functional check of the N > 1 path, not a timing
@@ -317,8 +317,9 @@ def run_ours(args):
         sim = Simulator(n, world_size=world, rank=rank, device=dev, nccl_uid=uid[0])
     elif "WORLD_SIZE" in os.environ and args.shards == 1:  # torchrun N=1: the per-rank API
         sim = Simulator(n, world_size=1, rank=0, device=dev)
-    else:
+    else:  # one process: --shards virtual shards, or --remap p2p over --gpus devices
         sim = Simulator(n, args.shards)
+    shards_total = world if world > 1 else args.shards
     stream = torch.cuda.Stream()          # a real stream: events on it bracket the kernels
     torch.cuda.set_stream(stream)
     sim.set_stream(stream.cuda_stream)
@@ -326,7 +327,7 @@ def run_ours(args):
     t_plan = time.perf_counter()
     plan = Plan(sim, c, nm, fuse=args.fuse, k_max=args.kmax, profile=True)
     plan_wall_ms = (time.perf_counter() - t_plan) * 1e3
-    counts = plan_counts(args.config, n, world, args.fuse, args.kmax)
+    counts = plan_counts(args.config, n, shards_total, args.fuse, args.kmax)
     pinfo = plan.info()
     if pinfo["gate_updates"] != counts["gate_updates"]:
         raise SystemExit(f"workloads/plan_counts.json is stale ({counts['gate_updates']} vs "
@@ -474,15 +475,21 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": (world if world > 1 else
+                       min(args.shards, torch.cuda.device_count()) if args.remap == "p2p" else 1),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, c, counts),
             "parallelism": (f"{world} ranks sharing GPU(s) through the NCCL test shim "
                             f"(functional check, not a timing)" if shim and world > 1 else
-                            f"state partitioned over {world} GPU(s) by high bits"
-                            if args.shards == 1 else
+                            f"state partitioned over {world} GPU(s) by high bits, one process "
+                            f"per GPU, NCCL remaps" if world > 1 else
+                            "1 GPU" if args.shards == 1 else
+                            f"{args.shards} shards in one process over "
+                            f"{min(args.shards, torch.cuda.device_count())} device(s), in-place "
+                            f"peer-to-peer remap swaps (--remap p2p)" if args.remap == "p2p" else
                             f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
             "plan": {"kernel_ops": st["ops_fused"],
                      "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
@@ -529,6 +536,10 @@ def main():
                     help="N=1: also run the whole config circuit at this n on the oracle beside "
                          "the GPU (default: 12 for config 4, else skipped; 0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--remap", default="nccl", choices=["nccl", "p2p"],
+                    help="--gpus N > 1: one process per GPU with NCCL point-to-point remaps "
+                         "(torchrun) or one process holding all N shards with in-place P2P swap "
+                         "kernels over peer memory")
     ap.add_argument("--shards", type=int, default=1,
                     help="N=1 only: split the state into this many virtual shards on the one GPU "
                          "(exercises the global-qubit remap with the in-place swap kernel)")
@@ -539,6 +550,9 @@ def main():
         args.whole_n = 12 if args.config == 4 else 0
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and args.remap == "p2p":
+        args.shards = args.gpus
+        return run_ours(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args)
     return run_ours(args)

@@ -30,7 +30,9 @@
 // epilogue additions:  k1 = a(c+d);  Re y = k1 - (a+b) d;  Im y = k1 + (b-a) c, where the
 // second and third products accumulate onto k1 (DMMA with C = k1).  a, -(a+b) and (b-a) are
 // precomputed fragments, so the only FP64 adds left are the c+d of each B element.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -95,6 +97,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, const int* c,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const int* c, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -142,7 +160,7 @@ __device__ __forceinline__ void piece_transpose(double2* P, int rot) {
 
 // k = 2 sub-op on one warp's half block.  F: fragments [3][4 ks][32 lanes][2 mt] doubles
 // (a, -(a+b), b-a); T: this lane's 32 offsets (16 B-fragment [ks][j], 16 D-fragment [mt][j][c]).
-template <int UI>
+template <int UI, int ACC>
 __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const uint16_t* T,
                                            int lane, int trow, int rows) {
   double a1[2][4], a2[2][4], a3[2][4];
@@ -194,22 +212,47 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
         for (int mt = 0; mt < 2; ++mt) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], sx);
       }
     double yr[UI][2][2], yi[UI][2][2];
-#pragma unroll
-    for (int u = 0; u < UI; ++u)
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb[u][0].y, k1[u][mt][0], k1[u][mt][1]);
-        dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb[u][0].x, k1[u][mt][0], k1[u][mt][1]);
-      }
-#pragma unroll
-    for (int ks = 1; ks < 4; ++ks)
+    if constexpr (ACC == 0) {  // seeded: Re/Im chains start from k1 (no epilogue adds)
 #pragma unroll
       for (int u = 0; u < UI; ++u)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
-          dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+          dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb[u][0].y, k1[u][mt][0], k1[u][mt][1]);
+          dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb[u][0].x, k1[u][mt][0], k1[u][mt][1]);
         }
+#pragma unroll
+      for (int ks = 1; ks < 4; ++ks)
+#pragma unroll
+        for (int u = 0; u < UI; ++u)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
+            dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+          }
+    } else {  // three independent chains (critical path 4 DMMA), 2 DADD per output
+#pragma unroll
+      for (int u = 0; u < UI; ++u)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) yr[u][mt][0] = yr[u][mt][1] = yi[u][mt][0] = yi[u][mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int u = 0; u < UI; ++u)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb[u][ks].y);
+            dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb[u][ks].x);
+          }
+#pragma unroll
+      for (int u = 0; u < UI; ++u)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            yr[u][mt][c] += k1[u][mt][c];
+            yi[u][mt][c] += k1[u][mt][c];
+          }
+    }
     __syncwarp();  // every lane's B loads of this pass precede any lane's D stores
 #pragma unroll
     for (int u = 0; u < UI; ++u)
@@ -271,7 +314,7 @@ static_assert(16 * kBlockMaxPairs + 64 * 8 + 64 * 2 <= kBlockHdrBytes, "block he
 // cp.async.cg copies (16 per thread, 16 lanes per piece: every warp instruction reads two
 // contiguous 256 B runs), signalled with cp.async.mbarrier.arrive, and store it back with
 // coalesced LDS + STG.128 -- no per-lane serialised bulk-copy issue.
-template <int UI, int COPY>
+template <int UI, int COPY, int ACC>
 __global__ void __launch_bounds__(384, 1)
     block_kernel(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -327,7 +370,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     const uint64_t base = insert_zeros10(i, p.lo_mask);
     const bool self = is_self(base);
-    if constexpr (COPY == 0) {
+    if constexpr (COPY == 0 || COPY == 2) {
       bool tr;
       const uint64_t src = piece_src(base, self, goff, tr);
       mbar_arrive_tx(bar, 256);
@@ -381,8 +424,8 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     pair_bar(pair);
-    if constexpr (COPY == 1) {
-      // the other stage was read out (LDS) by every pair thread before the barrier above
+    if constexpr (COPY == 1 || COPY == 2) {
+      // the other stage was read out (LDS for the stores) before the barrier above
       if (!first && nxt < nb) issue(nxt, s ^ 1);
     }
     if (!(p.dbg & 1)) {
@@ -394,7 +437,7 @@ __global__ void __launch_bounds__(384, 1)
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
+          blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
@@ -429,183 +472,241 @@ __global__ void __launch_bounds__(384, 1)
   if constexpr (COPY == 0) bulk_wait0();
 }
 
-// Warp-specialised variant (COPY = 2): 2 producer warps (the last two of the CTA) move every
-// block of 3 pairs each -- bulk G2S loads onto `full` mbarriers (arrive.expect_tx 16 KB) and bulk
-// S2G stores once the pair's 64 consumer threads have arrived on `done` -- so the consumer
-// warps run only fixups and the sub-op DMMA program.  A stage is refilled with the pair's block
-// k + 2 as soon as the bulk stores of block k have read it out (cp.async.bulk.wait_group.read).
+// TMA layout kernel (BlockParams::tma = 1).  Shared memory: mbarriers | blob (fragments,
+// tables, slot table) | 1024 B-aligned stages of 16 KB (box order, 128 B swizzle).  Per block:
+//   direct (every element stored in place: the base differs at a pair above hi_blk, or the
+//   full layout) -- pair thread 0 issues one TMA box load (arrive.expect_tx 16 KB, the other 63
+//   threads plain arrivals) and, after the sub-ops, one TMA box store;
+//   otherwise -- every pair thread issues 16 cp.async 16 B copies (16 lanes per 256 B piece)
+//   straight to each element's final slot (pieces read from the transposed position land
+//   already permuted), conjugates them after the wait, and stores them back with STG.
 template <int UI>
-__global__ void __launch_bounds__(448)
-    block_kernel_ws(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);  // full [2P] | done [2P]
-  uint64_t* sGoff = mbar + 4 * kBlockMaxPairs;
-  uint16_t* sStart = reinterpret_cast<uint16_t*>(sGoff + 64);
-  unsigned char* sBlob = smem_raw + kBlockHdrBytesWs;
-  double2* sStage = reinterpret_cast<double2*>(sBlob + p.blob_bytes);
+__global__ void __launch_bounds__(384, 1)
+    block_kernel_tma(double2* __restrict__ a, const __grid_constant__ BlockParams p,
+                     const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw);
+  unsigned char* sBlob = smem_raw + kBlockHdrBytes;
+  const size_t stage_off = (kBlockHdrBytes + (size_t)p.blob_bytes + 1023) & ~(size_t)1023;
+  double2* sStage = reinterpret_cast<double2*>(smem_raw + stage_off);
+  const uint16_t* sSlot = reinterpret_cast<const uint16_t*>(sBlob) + p.slot_off;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = p.pairs;
+  const int pair = warp >> 1, half = warp & 1, pt = threadIdx.x & 63;
   {
     const uint4* src = reinterpret_cast<const uint4*>(p.blob);
     uint4* dst = reinterpret_cast<uint4*>(sBlob);
     for (int i = threadIdx.x; i < p.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
-    if (threadIdx.x < 64) {
-      sGoff[threadIdx.x] = p.piece_goff[threadIdx.x];
-      sStart[threadIdx.x] = p.piece_start[threadIdx.x];
-    }
-    if (threadIdx.x < 2 * P) {
-      mbar_init(&mbar[threadIdx.x], 1);                   // full: the producer's expect_tx
-      mbar_init(&mbar[2 * kBlockMaxPairs + threadIdx.x], 64);  // done: the pair's threads
-    }
+    if (threadIdx.x < 2 * p.pairs) mbar_init(&mbar[threadIdx.x], 64);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (pair >= p.pairs) return;
+  double2* stage0 = sStage + (size_t)pair * 2 * 1024;
   const uint64_t nb = p.n_blocks;
-  const uint64_t npairs = (uint64_t)gridDim.x * P;
+  const uint64_t npairs = (uint64_t)gridDim.x * p.pairs;
   const bool mirror = p.mirror != 0;
   auto next_block = [&](uint64_t i) {
     if (mirror)
       while (i < nb && i > pair_swap64(i)) i += npairs;
     return i;
   };
-  auto is_self = [&](uint64_t base) { return mirror && pair_swap64(base) == base; };
-  auto piece_src = [&](uint64_t base, bool self, uint64_t go, bool& tr) {
-    const uint64_t e0 = base + go;
-    const uint64_t em = pair_swap64(e0);
-    tr = mirror && !self && e0 > em;
-    return tr ? em : e0;
+  // block classification: 0 direct (TMA), 1 cp.async with transposed pieces, 2 self-transposed
+  auto kind_of = [&](uint64_t base) {
+    if (!mirror) return 0;
+    const uint64_t d = (base ^ (base >> 1)) & 0x5555555555555555ull;
+    if (!d) return 2;
+    return (63 - __clzll(d)) > p.hi_blk ? 0 : 1;
   };
-  uint64_t* full = mbar;
-  uint64_t* done = mbar + 2 * kBlockMaxPairs;
-
-  if (warp >= 2 * P) {
-    // ------------------------------ producers ------------------------------
-    const int w = warp - 2 * P;  // 0 or 1: pairs w, w + 2, w + 4
-    auto load = [&](int pr, int st, uint64_t i) {
-      uint64_t* bar = &full[pr * 2 + st];
-      if (lane == 0) mbar_arrive_tx(bar, (p.dbg & 2) ? 0u : 16384u);
-      if (p.dbg & 2) return;
-      __syncwarp();
-      const uint64_t base = insert_zeros10(i, p.lo_mask);
-      const bool self = is_self(base);
-      double2* stg = sStage + ((size_t)pr * 2 + st) * kStageUnits;
+  auto coords = [&](uint64_t base, int* c) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = lane + 32 * h;
-        bool tr;
-        const uint64_t src = piece_src(base, self, sGoff[r], tr);
-        bulk_g2s(stg + sStart[r], a + src, 256, bar);
-      }
-    };
-    auto store = [&](int pr, int st, uint64_t i) {
-      if (p.dbg & 2) return;
-      const uint64_t base = insert_zeros10(i, p.lo_mask);
-      const bool self = is_self(base);
-      const double2* stg = sStage + ((size_t)pr * 2 + st) * kStageUnits;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = lane + 32 * h;
-        bool tr;
-        const uint64_t dst = piece_src(base, self, sGoff[r], tr);
-        bulk_s2g(a + dst, stg + sStart[r], 256);
-      }
-      bulk_commit();
-    };
-    uint64_t bk[3], b1[3], bk2[3];  // per served pair: blocks of iterations k, k+1, k+2
-    int prs[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      prs[j] = w + 2 * j;
-      const bool ok = prs[j] < P;
-      bk[j] = ok ? next_block((uint64_t)blockIdx.x * P + prs[j]) : nb;
-      b1[j] = bk[j] < nb ? next_block(bk[j] + npairs) : nb;
-      if (bk[j] < nb) load(prs[j], 0, bk[j]);
-      if (b1[j] < nb) load(prs[j], 1, b1[j]);
-      bk2[j] = b1[j] < nb ? next_block(b1[j] + npairs) : nb;
+    for (int d = 0; d < 5; ++d)
+      c[d] = d < p.tdims ? (int)((base >> p.tlo[d]) & (((uint64_t)1 << p.tbits[d]) - 1)) : 0;
+    c[0] *= 2;  // dim 0 counts doubles
+  };
+  auto issue = [&](uint64_t i, int s) {
+    uint64_t* bar = &mbar[pair * 2 + s];
+    double2* st = stage0 + s * 1024;
+    if (p.dbg & 2) {
+      mbar_arrive(bar);
+      return;
     }
-    for (uint32_t k = 0;; ++k) {
-      const int st = k & 1;
-      const uint32_t par = (k >> 1) & 1;
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        if (bk[j] >= nb) continue;
-        any = true;
-        mbar_wait(&done[prs[j] * 2 + st], par);
-        store(prs[j], st, bk[j]);
+    const uint64_t base = insert_zeros10(i, p.lo_mask);
+    const int kd = kind_of(base);
+    if (kd == 0) {
+      if (pt == 0) {
+        mbar_arrive_tx(bar, 16384);
+        int c[5];
+        coords(base, c);
+        tma_load_5d(st, &tmap, c, bar);
+      } else {
+        mbar_arrive(bar);
       }
-      if (!any) break;
-      bulk_wait_read0();  // the stores above have read their stages out
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        if (bk[j] >= nb) continue;
-        if (bk2[j] < nb) load(prs[j], st, bk2[j]);
-        // iteration k + 1 handles b_{k+1}; b_{k+3} follows b_{k+2}
-        const uint64_t nk = b1[j];
-        b1[j] = bk2[j];
-        bk2[j] = bk2[j] < nb ? next_block(bk2[j] + npairs) : nb;
-        bk[j] = nk;
+    } else {
+      const int u = pt & 15, qb = pt >> 4;
+#pragma unroll 4
+      for (int it = 0; it < 16; ++it) {
+        const int q = it * 4 + qb;
+        const uint64_t e0 = base + p.piece_goff[q];
+        const uint64_t em = pair_swap64(e0);
+        const bool tr = kd == 1 && e0 > em;
+        cp_async16_cg(st + sSlot[q * 16 + (tr ? pswap4(u) : u)], a + (tr ? em : e0) + u);
       }
+      cp_async_mbar_arrive(bar);
     }
-    bulk_wait0();
-    return;
-  }
+  };
 
-  // ------------------------------ consumers ------------------------------
-  const int pair = warp >> 1, half = warp & 1, pt = threadIdx.x & 63;
-  double2* stage0 = sStage + (size_t)pair * 2 * kStageUnits;
-  const uint64_t goff = sGoff[pt];
-  const int sstart = sStart[pt];
-  const int rot = piece_rot(pt & 7);
-  uint64_t cur = next_block((uint64_t)blockIdx.x * P + pair);
-  for (uint32_t k = 0; cur < nb; ++k) {
-    const int st = k & 1;
-    double2* X = stage0 + st * kStageUnits;
-    mbar_wait(&full[pair * 2 + st], (k >> 1) & 1);
+  uint64_t cur = next_block((uint64_t)blockIdx.x * p.pairs + pair);
+  uint64_t nxt = cur < nb ? next_block(cur + npairs) : nb;
+  if (cur < nb) issue(cur, 0);
+  if (nxt < nb) issue(nxt, 1);
+  uint32_t parity[2] = {0u, 0u};
+  bool first = true;
+  int s = 0;
+  while (cur < nb) {
+    double2* X = stage0 + s * 1024;
+    mbar_wait(&mbar[pair * 2 + s], parity[s]);
+    parity[s] ^= 1u;
+    if (pt == 0 && !first) bulk_wait_read0();  // last iteration's TMA store has read its stage
     const uint64_t base = insert_zeros10(cur, p.lo_mask);
-    const bool self = is_self(base);
-    bool trp;
-    piece_src(base, self, goff, trp);
-    if (trp) piece_transpose(X + sstart, rot);
-    if (self) {
-      for (int kk = 0; kk < 16; ++kk) {
-        const int idx = pt * 16 + ((kk + pt) & 15);
+    const int kd = (p.dbg & 2) ? 0 : kind_of(base);
+    if (kd == 1) {  // conjugate the pieces that came from the transposed position
+      const uint64_t e0 = base + p.piece_goff[pt];
+      if (e0 > pair_swap64(e0)) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          double* im = &X[sSlot[pt * 16 + ((t + pt) & 15)]].y;
+          *im = -*im;
+        }
+      }
+    } else if (kd == 2) {  // self-transposed: non-canonical <- conj(canonical)
+      for (int k = 0; k < 16; ++k) {
+        const int idx = pt * 16 + ((k + pt) & 15);
         const int idm = ((idx & 0x155) << 1) | ((idx >> 1) & 0x155);
         if (idx > idm) {
-          const double2 v = X[p.start_by_pidx[idm >> 4] + (idm & 15)];
-          X[p.start_by_pidx[idx >> 4] + (idx & 15)] = make_double2(v.x, -v.y);
+          const double2 v = X[sSlot[idm]];
+          X[sSlot[idx]] = make_double2(v.x, -v.y);
         }
       }
     }
     pair_bar(pair);
+    if (!first && nxt < nb) issue(nxt, s ^ 1);
     if (!(p.dbg & 1)) {
-      const bool shared_tab = p.half_add >= 0;
-      double2* Xh = X + (shared_tab ? half * p.half_add : 0);
-      const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
+      double2* Xh = X;
+      const int trow = half * 32 + lane;
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI>(Xh, F, T, lane, trow, trows);
+          blk_sub_k2<UI, 0>(Xh, F, T, lane, trow, 64);
         else
-          blk_sub_k1(Xh, F, T, trow, trows);
+          blk_sub_k1(Xh, F, T, trow, 64);
         __syncwarp();
       }
     }
+    if (kd == 0) fence_async_smem();
     pair_bar(pair);
-    if (trp) piece_transpose(X + sstart, rot);
-    fence_async_smem();
-    mbar_arrive(&done[pair * 2 + st]);
-    cur = next_block(cur + npairs);
+    if (!(p.dbg & 2)) {
+      if (kd == 0) {
+        if (pt == 0) {
+          int c[5];
+          coords(base, c);
+          tma_store_5d(&tmap, c, X);
+          bulk_commit();
+        }
+      } else {
+        const int u = pt & 15, qb = pt >> 4;
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int q = it * 4 + qb;
+          const uint64_t e0 = base + p.piece_goff[q];
+          const uint64_t em = pair_swap64(e0);
+          const bool tr = kd == 1 && e0 > em;
+          double2 v = X[sSlot[q * 16 + (tr ? pswap4(u) : u)]];
+          if (tr) v.y = -v.y;
+          a[(tr ? em : e0) + u] = v;
+        }
+      }
+    }
+    first = false;
+    cur = nxt;
+    nxt = cur < nb ? next_block(cur + npairs) : nb;
+    s ^= 1;
   }
+  if (pt == 0) bulk_wait0();
 }
 
-template <int UI, int COPY>
+size_t block_smem_bytes_tma(int pairs, int blob_bytes) {
+  return ((kBlockHdrBytes + (size_t)blob_bytes + 1023) & ~(size_t)1023) + (size_t)pairs * 2 * 16384;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+static cudaError_t encode_block_tmap(CUtensorMap* map, double2* a, const BlockParams& p) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t box[5], estride[5] = {1, 1, 1, 1, 1};
+  const int top = p.tlo[p.tdims - 1] + p.tbits[p.tdims - 1];  // = local bits L
+  for (int d = 0; d < 5; ++d) {
+    if (d < p.tdims) {
+      gdim[d] = (cuuint64_t)1 << p.tbits[d];
+      box[d] = 1u << p.tbox[d];
+    } else {  // unit padding dims beyond the whole shard
+      gdim[d] = 1;
+      box[d] = 1;
+    }
+    if (d >= 1) gstride[d - 1] = (cuuint64_t)16 << (d < p.tdims ? p.tlo[d] : top);
+  }
+  gdim[0] *= 2;  // doubles
+  box[0] *= 2;
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a, gdim, gstride, box, estride,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+static cudaError_t launch_block_tma(double2* a, const BlockParams& p, cudaStream_t st) {
+  static std::atomic<uint64_t> attr_done{0};
+  auto kern = block_kernel_tma<2>;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = (uint64_t)1 << (dev & 63);
+  if (!(attr_done.load() & bit)) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done.fetch_or(bit);
+  }
+  CUtensorMap map;
+  e = encode_block_tmap(&map, a, p);
+  if (e != cudaSuccess) {
+    set_error("cuTensorMapEncodeTiled rejected the block box");
+    return e;
+  }
+  const size_t smem = block_smem_bytes_tma(p.pairs, p.blob_bytes);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (p.n_blocks + p.pairs - 1) / p.pairs;
+  unsigned grid = (unsigned)(want < (uint64_t)sms ? want : (uint64_t)sms);
+  const char* cap = getenv("TANQ_GRID_CAP");
+  if (cap && atoi(cap) > 0 && grid > (unsigned)atoi(cap)) grid = (unsigned)atoi(cap);
+  if (grid < 1) grid = 1;
+  kern<<<grid, 64 * p.pairs, smem, st>>>(a, p, map);
+  return cudaGetLastError();
+}
+
+template <int UI, int COPY, int ACC>
 static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t smem,
                                     cudaStream_t st) {
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = block_kernel<UI, COPY>;
+  auto kern = block_kernel<UI, COPY, ACC>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -630,54 +731,32 @@ size_t block_smem_bytes(int pairs, int blob_bytes) {
   return kBlockHdrBytes + (size_t)blob_bytes + (size_t)pairs * 2 * kStageUnits * 16;
 }
 
-// env TANQ_BLOCK_COPY = bulk (default) | ws (warp-specialised producers) | ldg: how blocks move
-// between HBM and shared memory.  Measured at n = 16 (profiles/r02_block_copy_variants.txt):
-// bulk 15.5-17.7 ms per 2-sub-op group, ldg 16.7-21.4, ws 33 (2 producer warps cannot issue
-// 256 B bulk copies fast enough: ~65 clock cycles per copy per warp).
-cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st) {
-  static int copy = -1;
+// env TANQ_BLOCK_COPY = bulk (default) | ldg | bs: how blocks move between HBM and shared
+// memory -- bulk: cp.async.bulk pieces both ways; ldg: 16 B cp.async loads + coalesced STG
+// stores; bs: bulk loads + STG stores.  A warp-specialised producer variant (2 producer warps
+// issuing every piece) and a single-elected-thread issue loop were measured slower and removed
+// (profiles/r02_block_copy_variants.txt).  TANQ_BLOCK_ACC = 1: three independent DMMA
+// accumulators + 2 DADD per output instead of the seeded chain.
+cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStream_t st) {
+  (void)L;
+  if (p.tma) return launch_block_tma(a, p, st);
+  static int copy = -1, acc = -1;
   if (copy < 0) {
     const char* e = getenv("TANQ_BLOCK_COPY");
-    copy = !e ? 0 : (e[0] == 'w' ? 2 : (e[0] == 'l' ? 1 : 0));
+    copy = !e ? 0 : (e[0] == 'l' ? 1 : (!strcmp(e, "bs") ? 2 : 0));
+    const char* f = getenv("TANQ_BLOCK_ACC");
+    acc = (f && f[0] == '1') ? 1 : 0;
   }
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
-  if (copy == 2) {
-    static std::atomic<uint64_t> attr_done{0};
-    auto kern = block_kernel_ws<2>;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    const uint64_t bit = (uint64_t)1 << (dev & 63);
-    if (!(attr_done.load() & bit)) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (e != cudaSuccess) return e;
-      attr_done.fetch_or(bit);
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t want = (p.n_blocks + p.pairs - 1) / p.pairs;
-    unsigned grid = (unsigned)(want < (uint64_t)sms ? want : (uint64_t)sms);
-    const char* cap = getenv("TANQ_GRID_CAP");
-    if (cap && atoi(cap) > 0 && grid > (unsigned)atoi(cap)) grid = (unsigned)atoi(cap);
-    if (grid < 1) grid = 1;
-    kern<<<grid, 64 * p.pairs + 64, smem, st>>>(a, p);
-    e = cudaGetLastError();
-    if (e == cudaErrorLaunchOutOfResources) {  // diagnostics for the error message
-      cudaFuncAttributes fa;
-      if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-        char msg[256];
-        snprintf(msg, sizeof msg,
-                 "block_kernel_ws: %d threads, %zu B dynamic smem; kernel: %d regs, max %d "
-                 "threads, %zu B static smem, %zu B local",
-                 64 * p.pairs + 64, smem, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
-                 fa.localSizeBytes);
-        set_error(msg);
-      }
-    }
-    return e;
+  if (acc == 1) {
+    if (copy == 1) return launch_block_cfg<2, 1, 1>(a, p, smem, st);
+    if (copy == 2) return launch_block_cfg<2, 2, 1>(a, p, smem, st);
+    return launch_block_cfg<2, 0, 1>(a, p, smem, st);
   }
-  return copy == 0 ? launch_block_cfg<2, 0>(a, p, smem, st) : launch_block_cfg<2, 1>(a, p, smem, st);
+  if (copy == 1) return launch_block_cfg<2, 1, 0>(a, p, smem, st);
+  if (copy == 2) return launch_block_cfg<2, 2, 0>(a, p, smem, st);
+  return launch_block_cfg<2, 0, 0>(a, p, smem, st);
 }
 
 }  // namespace tanq

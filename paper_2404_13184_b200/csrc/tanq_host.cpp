@@ -1141,9 +1141,9 @@ bool block_enabled() {
 
 size_t block_sub_bytes(int k) { return k == 2 ? 768 * 8 + 2 * 32 * 32 * 2 : 32 * 8 + 2 * 32 * 16 * 2; }
 
-size_t block_blob_bytes(const FusedOp& op) {
-  size_t b = 0;
-  if (op.sub.empty()) return block_sub_bytes(op.k);
+size_t block_blob_bytes(const FusedOp& op) {  // upper bound (incl. the TMA slot table)
+  size_t b = 2048;
+  if (op.sub.empty()) return b + block_sub_bytes(op.k);
   for (const auto& sb : op.sub) b += block_sub_bytes(sb.k);
   return b;
 }
@@ -1179,13 +1179,26 @@ size_t prog_capacity(const FusedOp& op) {
   return std::max(group_prog_elems(op), (block_blob_bytes(op) + 15) / 16);
 }
 
-int phase_degree(int w0, int w1, int w2) {  // max lanes per bank over the 8 combinations
+// max lanes per bank over the 8 lane combinations of a quarter warp whose 3 varying index bits
+// have bank contributions w0, w1, w2: added mod 8 (rotation layout) or XORed (TMA swizzle)
+bool g_bank_xor = false;  // set by build_block while it evaluates a layout
+int phase_degree(int w0, int w1, int w2) {
   int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
   for (int c = 0; c < 8; ++c) {
-    const int b = ((c & 1 ? w0 : 0) + (c & 2 ? w1 : 0) + (c & 4 ? w2 : 0)) & 7;
+    const int b = g_bank_xor ? ((c & 1 ? w0 : 0) ^ (c & 2 ? w1 : 0) ^ (c & 4 ? w2 : 0))
+                             : ((c & 1 ? w0 : 0) + (c & 2 ? w1 : 0) + (c & 4 ? w2 : 0)) & 7;
     mx = std::max(mx, ++cnt[b]);
   }
   return mx;
+}
+
+int block_tma_mode() {  // env TANQ_BLOCK_TMA = 0 (never) | 1 (whenever possible) | auto
+  static int m = -1;
+  if (m < 0) {
+    const char* e = std::getenv("TANQ_BLOCK_TMA");
+    m = !e ? 2 : (e[0] == '0' ? 0 : (e[0] == '1' ? 1 : 2));
+  }
+  return m;
 }
 
 // Zero-tile skipping (BlockSub::tmask) measured slower on B200 (uniform branches around the
@@ -1360,6 +1373,73 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
         if (c < cost) cost = c;
         else w[j] = old;
       }
+  // TMA layout: the block as a box of <= 5 dims (runs of block bits + the gap above each run,
+  // bits 0-2 as the 128 B inner dim) landing in box order with the 128 B swizzle.  The dims
+  // after the inner one may come in any order: their first three box bits are the swizzle's row
+  // bits (XORed into the bank), so the order is chosen for the fewest bank conflicts.  Bank
+  // contributions XOR: bits 0-2 -> 1, 2, 4; the first three row bits -> 1, 2, 4; others none.
+  bool use_tma = false;
+  int tdims = 0, tlo[5] = {0, 0, 0, 0, 0}, tbits[5] = {0, 0, 0, 0, 0}, tbox[5] = {0, 0, 0, 0, 0};
+  int sbit[10];  // TMA layout: box-linear bit of block bit j
+  {
+    std::vector<std::pair<int, int>> runs;  // block-bit runs above bit 2: (first block bit, length)
+    for (int j = 3; j < 10; ++j) {
+      if (!runs.empty() && bpos[runs.back().first] + runs.back().second == bpos[j]) ++runs.back().second;
+      else runs.push_back({j, 1});
+    }
+    if (runs.size() <= 4 && block_tma_mode() != 0) {
+      std::vector<int> ord(runs.size());
+      for (size_t r = 0; r < ord.size(); ++r) ord[r] = (int)r;
+      int best_cost = 1 << 30;
+      std::vector<int> best_ord = ord;
+      int wx[10];
+      do {
+        int pos = 3;
+        for (int j = 0; j < 3; ++j) wx[j] = 1 << j;
+        for (int r : ord)
+          for (int b = 0; b < runs[r].second; ++b, ++pos)
+            wx[runs[r].first + b] = pos < 6 ? 1 << (pos - 3) : 0;
+        g_bank_xor = true;
+        const int c = total_cost(wx);
+        g_bank_xor = false;
+        if (c < best_cost) {
+          best_cost = c;
+          best_ord = ord;
+        }
+      } while (std::next_permutation(ord.begin(), ord.end()));
+      tdims = 1 + (int)runs.size();
+      tlo[0] = 0; tbits[0] = 3; tbox[0] = 3;
+      int pos = 3;
+      for (int j = 0; j < 3; ++j) sbit[j] = j;
+      for (size_t d = 0; d < best_ord.size(); ++d) {
+        const int r = best_ord[d];
+        const int first = bpos[runs[r].first];
+        tlo[d + 1] = first;
+        tbox[d + 1] = runs[r].second;
+        const int next = (size_t)r + 1 < runs.size() ? bpos[runs[r + 1].first] : s->L;
+        tbits[d + 1] = next - first;
+        for (int b = 0; b < runs[r].second; ++b, ++pos) {
+          sbit[runs[r].first + b] = pos;
+          wx[runs[r].first + b] = pos < 6 ? 1 << (pos - 3) : 0;
+        }
+      }
+      for (int j = 0; j < 3; ++j) wx[j] = 1 << j;
+      // packed layout: blocks are moved by one TMA only when no member pair decides where an
+      // element is stored, i.e. the base differs at a qubit above the group -- require the
+      // highest block bit to leave at least two qubits above it (>= 15/16 of the blocks)
+      const bool mostly_direct = !use_mirror(s, op) || bpos[9] + 4 < s->L;
+      use_tma = block_tma_mode() == 1 || (mostly_direct && best_cost <= cost);
+      if (std::getenv("TANQ_BLOCK_DEBUG"))
+        std::fprintf(stderr, "block q=%d,%d,%d dims=%d cost rot %d tma %d direct %d -> %s\n",
+                     op.q[0], op.q[1], op.k > 2 ? op.q[2] : -1, tdims, cost, best_cost,
+                     (int)mostly_direct, use_tma ? "tma" : "rot");
+      if (use_tma) {
+        for (int j = 0; j < 10; ++j) w[j] = wx[j];
+        cost = best_cost;
+      }
+    }
+  }
+  if (use_tma) g_bank_xor = true;
   // placement: pieces sorted by G, piece at 16 * rank + G
   int G[64], order[64];
   for (int pi = 0; pi < 64; ++pi) {
@@ -1369,11 +1449,11 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     G[pi] = g & 7;
     order[pi] = pi;
   }
-  std::stable_sort(order, order + 64, [&](int x, int y) { return G[x] < G[y]; });
+  if (!use_tma) std::stable_sort(order, order + 64, [&](int x, int y) { return G[x] < G[y]; });
   int start_by_pidx[64];
   for (int r = 0; r < 64; ++r) {
     const int pi = order[r];
-    start_by_pidx[pi] = 16 * r + G[pi];
+    start_by_pidx[pi] = use_tma ? 16 * pi : 16 * r + G[pi];  // TMA: slot() applies the swizzle
     uint64_t off = 0;
     for (int b = 0; b < 6; ++b)
       if ((pi >> b) & 1) off += (uint64_t)1 << bpos[4 + b];
@@ -1381,7 +1461,21 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     p.piece_start[r] = (uint16_t)start_by_pidx[pi];
   }
   for (int pi = 0; pi < 64; ++pi) p.start_by_pidx[pi] = (uint16_t)start_by_pidx[pi];
-  auto slot = [&](int idx) { return start_by_pidx[idx >> 4] + (idx & 15); };
+  auto slot = [&](int idx) {
+    if (!use_tma) return start_by_pidx[idx >> 4] + (idx & 15);
+    int sidx = 0;  // box-linear index, then the 128 B swizzle
+    for (int j = 0; j < 10; ++j)
+      if ((idx >> j) & 1) sidx |= 1 << sbit[j];
+    return sidx ^ ((sidx >> 3) & 7);
+  };
+  p.tma = use_tma ? 1u : 0u;
+  p.tdims = tdims;
+  for (int d = 0; d < 5; ++d) {
+    p.tlo[d] = tlo[d];
+    p.tbits[d] = tbits[d];
+    p.tbox[d] = tbox[d];
+  }
+  p.hi_blk = bpos[9];
   for (int j = 0; j < 10; ++j) p.lo_mask[j] = ((uint64_t)1 << bpos[j]) - 1;
   p.n_blocks = (uint64_t)1 << (s->L - 10);
   p.mirror = use_mirror(s, op) ? 1u : 0u;
@@ -1393,8 +1487,9 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   p.dbg = (uint32_t)dbg;
   p.n_sub = (int)subs.size();
   // the warp-half bit is in-piece bit 3 (both halves' offsets differ by 8 units): one table
-  const int halves = half == 3 ? 1 : 2;
-  p.half_add = half == 3 ? 8 : -1;
+  const bool share = half == 3 && !use_tma;
+  const int halves = share ? 1 : 2;
+  p.half_add = share ? 8 : -1;
   // blob: per sub-op fragments then tables (both 16 B aligned)
   size_t off = 0;
   for (size_t i = 0; i < subs.size(); ++i) {
@@ -1493,6 +1588,15 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       off += (size_t)halves * 32 * 16 * 2;
     }
   }
+  if (use_tma) {  // slot table for the cp.async path of blocks that are not moved by TMA
+    p.slot_off = (int)(off / 2);
+    uint16_t* st = reinterpret_cast<uint16_t*>(blob + off);
+    for (int idx = 0; idx < 1024; ++idx) st[idx] = (uint16_t)slot(idx);
+    off += 2048;
+  } else {
+    p.slot_off = -1;
+  }
+  g_bank_xor = false;
   p.blob_bytes = (int)off;
   p.pairs = block_pairs_for(off);
   return off;
@@ -1556,7 +1660,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
         tanq::BlockParams p = *bp;
         p.blob = (*prog)[di];
         g_err.clear();
-        const cudaError_t be = tanq::launch_block_group(sh.data, p, sh.stream);
+        const cudaError_t be = tanq::launch_block_group(sh.data, p, s->L, sh.stream);
         if (be != cudaSuccess)
           return fail(TANQ_E_CUDA, std::string("launch_block_group -> ") + cudaGetErrorString(be) +
                                        (g_err.empty() ? "" : " [" + g_err + "]"));

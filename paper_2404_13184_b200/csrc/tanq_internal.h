@@ -75,6 +75,19 @@ struct BlockParams {
   uint16_t piece_start[64];  // its shared-memory start (16 B units) in a stage
   uint16_t start_by_pidx[64];// shared-memory start of piece index (block bits 4..9)
   BlockSub sub[kBlockMaxSub];
+  // TMA layout (tma = 1): the block is described as a <= 5-D box of the shard -- dim d covers
+  // physical bits [tlo[d], tlo[d] + tbits[d]), its lowest tbox[d] bits vary inside the block --
+  // and lands in shared memory in box order with the 128 B swizzle: element idx (block order)
+  // at 16 B unit idx ^ ((idx >> 3) & 7).  Blocks whose elements are all stored in place (no
+  // pair above hi_blk needed to decide, not self-transposed) move with one TMA load / store;
+  // the others with 16 B cp.async copies placed through the slot table.
+  uint32_t tma;
+  int32_t tdims;
+  int32_t tlo[5];
+  int32_t tbits[5];
+  int32_t tbox[5];
+  int32_t hi_blk;            // highest block bit position
+  int32_t slot_off;          // uint16 offset of the 1024-entry slot table in the blob
 };
 
 struct BitMap {               // physical bit of each logical bit (row q -> 2q, col q -> 2q+1)
@@ -86,7 +99,7 @@ struct BitMap {               // physical bit of each logical bit (row q -> 2q, 
 cudaError_t launch_gate1(double2* a, const GateParams<1>& p, cudaStream_t st);
 cudaError_t launch_gate2(double2* a, const GateParams<2>& p, cudaStream_t st);
 cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st);
-cudaError_t launch_block_group(double2* a, const BlockParams& p, cudaStream_t st);
+cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStream_t st);
 size_t block_smem_bytes(int pairs, int blob_bytes);
 // packed Hermitian layout -> full layout (single shard, interleaved identity bit map)
 cudaError_t launch_unpack(double2* a, int L, cudaStream_t st);

@@ -89,7 +89,10 @@ class tanq_block_params(ctypes.Structure):
                 ("dbg", ctypes.c_uint32), ("half_add", ctypes.c_int32),
                 ("n_blocks", ctypes.c_uint64), ("lo_mask", ctypes.c_uint64 * 10),
                 ("piece_goff", ctypes.c_uint64 * 64), ("piece_start", ctypes.c_uint16 * 64),
-                ("start_by_pidx", ctypes.c_uint16 * 64), ("sub", tanq_block_sub * 12)]
+                ("start_by_pidx", ctypes.c_uint16 * 64), ("sub", tanq_block_sub * 12),
+                ("tma", ctypes.c_uint32), ("tdims", ctypes.c_int32), ("tlo", ctypes.c_int32 * 5),
+                ("tbits", ctypes.c_int32 * 5), ("tbox", ctypes.c_int32 * 5),
+                ("hi_blk", ctypes.c_int32), ("slot_off", ctypes.c_int32)]
 
 
 class tanq_info(ctypes.Structure):

@@ -53,7 +53,30 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
     mirror = bool(prm.mirror)
     dbl = blob.view(np.float64)
     u16 = blob.view(np.uint16)
-    assert sorted(start) == sorted(sbp)
+    tma = bool(getattr(prm, "tma", 0))
+    if tma:   # box order (dims as the tensor map lists them) + 128 B swizzle
+        tab = u16[int(prm.slot_off):int(prm.slot_off) + 1024]
+        assert sorted(int(x) for x in tab) == list(range(1024))
+        # the slot table must be the box order of the tensor-map dims, swizzled: rebuild it
+        pos_of = []            # physical position of block bit j
+        for j in range(10):
+            m = int(prm.lo_mask[j])
+            pos_of.append((m + 1).bit_length() - 1)
+        sb = [0, 1, 2] + [None] * 7
+        nxt = 3
+        for d in range(1, int(prm.tdims)):
+            for b in range(int(prm.tbox[d])):
+                j = pos_of.index(int(prm.tlo[d]) + b)
+                sb[j] = nxt
+                nxt += 1
+        def slot(idx):
+            s_ = sum(1 << sb[j] for j in range(10) if (idx >> j) & 1)
+            return s_ ^ ((s_ >> 3) & 7)
+        assert all(int(tab[i]) == slot(i) for i in range(1024))
+    else:
+        def slot(idx):
+            return sbp[idx >> 4] + (idx & 15)
+        assert sorted(start) == sorted(sbp)
     for i in range(int(prm.n_blocks)):
         if mirror and i > pair_swap(i):
             continue
@@ -66,17 +89,16 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
             em = pair_swap(e0)
             tr = mirror and not self_t and e0 > em
             src = em if tr else e0
-            st[start[j]:start[j] + 16] = a[src:src + 16]
-            trs.append((tr, src))
-            if tr:
-                piece = st[start[j]:start[j] + 16].copy()
-                for t in range(16):
-                    st[start[j] + pswap_bits(t, 4)] = np.conj(piece[t])
+            pidx = j if tma else [q for q in range(64) if sbp[q] == start[j]][0]
+            for t in range(16):   # element t of the loaded piece -> its block slot
+                tt = pswap_bits(t, 4) if tr else t
+                st[slot(pidx * 16 + tt)] = np.conj(a[src + t]) if tr else a[src + t]
+            trs.append((tr, src, pidx))
         if self_t:
             for idx in range(1024):
                 idm = pswap_bits(idx, 10)
                 if idx > idm:
-                    st[sbp[idx >> 4] + (idx & 15)] = np.conj(st[sbp[idm >> 4] + (idm & 15)])
+                    st[slot(idx)] = np.conj(st[slot(idm)])
         for q in range(int(prm.n_sub)):
             g = prm.sub[q]
             for h in range(2):
@@ -131,10 +153,9 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                     if check:
                         assert len(set(rd)) == 512
         for j in range(64):
-            tr, src = trs[j]
-            piece = st[start[j]:start[j] + 16].copy()
-            if tr:
-                for t in range(16):
-                    piece[pswap_bits(t, 4)] = np.conj(st[start[j] + t])
-            a[src:src + 16] = piece
+            tr, src, pidx = trs[j]
+            for t in range(16):
+                tt = pswap_bits(t, 4) if tr else t
+                v = st[slot(pidx * 16 + tt)]
+                a[src + t] = np.conj(v) if tr else v
     return a

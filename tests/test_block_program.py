@@ -147,3 +147,18 @@ def test_block_program_standalone_k2():
                                                              "tests": here}],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+def test_block_program_tma_layout_forced():
+    """TANQ_BLOCK_TMA=1: every block program uses the TMA box layout (dims in the chosen
+    order, 128 B swizzle, slot table for the cp.async path); the emulation must still match."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, TANQ_BLOCK_TMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_block_program.py"), "-k",
+                        "emulation_matches_oracle or standalone_k2"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

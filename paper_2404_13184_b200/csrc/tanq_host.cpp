@@ -1387,6 +1387,19 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       if (!runs.empty() && bpos[runs.back().first] + runs.back().second == bpos[j]) ++runs.back().second;
       else runs.push_back({j, 1});
     }
+    // split runs at qubit boundaries while dims remain, so the order search can choose which
+    // qubit's bits become the swizzle row bits
+    for (bool split = true; split && runs.size() < 4;) {
+      split = false;
+      for (size_t r = 0; r < runs.size() && !split; ++r)
+        for (int b = 1; b < runs[r].second; ++b)
+          if ((bpos[runs[r].first + b] & 1) == 0) {  // a qubit's row bit starts here
+            runs.insert(runs.begin() + r + 1, {runs[r].first + b, runs[r].second - b});
+            runs[r].second = b;
+            split = true;
+            break;
+          }
+    }
     if (runs.size() <= 4 && block_tma_mode() != 0) {
       std::vector<int> ord(runs.size());
       for (size_t r = 0; r < ord.size(); ++r) ord[r] = (int)r;
@@ -1425,10 +1438,16 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       }
       for (int j = 0; j < 3; ++j) wx[j] = 1 << j;
       // packed layout: blocks are moved by one TMA only when no member pair decides where an
-      // element is stored, i.e. the base differs at a qubit above the group -- require the
-      // highest block bit to leave at least two qubits above it (>= 15/16 of the blocks)
+      // element is stored, i.e. the base differs at a qubit above the group -- require at least
+      // two qubits above the group (about 3/4 of the processed blocks or more); the others go
+      // through the cp.async path
       const bool mostly_direct = !use_mirror(s, op) || bpos[9] + 4 < s->L;
-      use_tma = block_tma_mode() == 1 || (mostly_direct && best_cost <= cost);
+      static int slack = -1;
+      if (slack < 0) {
+        const char* e = std::getenv("TANQ_BLOCK_TMA_SLACK");
+        slack = e ? std::atoi(e) : 1;
+      }
+      use_tma = block_tma_mode() == 1 || (mostly_direct && best_cost <= cost + slack);
       if (std::getenv("TANQ_BLOCK_DEBUG"))
         std::fprintf(stderr, "block q=%d,%d,%d dims=%d cost rot %d tma %d direct %d -> %s\n",
                      op.q[0], op.q[1], op.k > 2 ? op.q[2] : -1, tdims, cost, best_cost,

@@ -20,11 +20,11 @@ print("ran", flush=True)
 '
 TOOLS=${TOOLS:-racecheck synccheck memcheck}
 for tool in $TOOLS; do
-  for v in "block auto 1" "block auto 0"  "warp direct 1" "q1 tile 1" "o1 auto 1" "auto auto 1" "auto auto 0" "warp tile 0"; do
+  for v in "block auto 1" "block auto 0" "blocktma auto 1" "blocktma auto 0" "warp direct 1" "q1 tile 1" "o1 auto 1" "auto auto 1" "auto auto 0" "warp tile 0"; do
     set -- $v
     echo "=== $tool TANQ_GROUP=$1 TANQ_K2PATH=$2 TANQ_MIRROR=$3 TANQ_GRID_CAP=2"
-    BLK=0; [ "$1" = block ] && BLK=1
-    TANQ_BLOCK=$BLK TANQ_GROUP=$1 TANQ_K2PATH=$2 TANQ_MIRROR=$3 TANQ_GRID_CAP=2 timeout 900 \
+    BLK=0; TMA=auto; [ "$1" = block ] && BLK=1 && TMA=0; [ "$1" = blocktma ] && BLK=1 && TMA=1
+    TANQ_BLOCK=$BLK TANQ_BLOCK_TMA=$TMA TANQ_GROUP=$1 TANQ_K2PATH=$2 TANQ_MIRROR=$3 TANQ_GRID_CAP=2 timeout 900 \
       /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 \
       python -c "$SNIP" > /tmp/san.$$ 2>&1
     grep -E 'Race reported|Error|Invalid|SUMMARY|^ran' /tmp/san.$$ | sed -E 's/\+0x[0-9a-f]+//' | sort | uniq -c | head -20

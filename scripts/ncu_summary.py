@@ -50,9 +50,10 @@ def main():
     ap.add_argument("--name-map", default="gate_kernel<1=gate_k1,gate_kernel<2=gate_k2,gate2_mma=gate_k2,group_kernel=group_dmma")
     args = ap.parse_args()
     nmap = [kv.split("=") for kv in args.name_map.split(",")]
-    traffic = json.load(open(args.traffic)) if os.path.exists(args.traffic) else {}
+    traffic = json.load(open(args.traffic)) if os.path.exists(args.traffic) else {}  # merged
     lines = ["| kernel | " + " | ".join(k[1] for k in KEYS) + " |",
              "|---|" + "---|" * len(KEYS)]
+    seen = set()
     for rep in args.reps:
         for hdr, units, r in rows_of(rep):
             col = {h: i for i, h in enumerate(hdr)}
@@ -67,6 +68,9 @@ def main():
                 tb = to_bytes(r[rd], units[rd]) + to_bytes(r[wr], units[wr])
                 for pat, short in nmap:
                     if pat in name:
+                        if short in seen:
+                            continue
+                        seen.add(short)
                         alg = args.bytes_per_amp * 4 ** args.n
                         traffic[short] = {"dram_bytes_per_launch": tb, "algorithmic_bytes_per_launch": alg,
                                           "ratio": tb / alg, "n_qubits": args.n,

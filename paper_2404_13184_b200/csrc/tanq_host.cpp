@@ -1156,11 +1156,14 @@ int block_pairs_for(size_t blob_bytes) {
 
 // Ops the block kernel runs: 3-qubit groups of k <= 2 sub-ops (not dense k = 3 ops), at least
 // 4 blocks, small enough programs.  Env TANQ_BLOCK=0 restores the round-1 group kernels.
-bool block_k2_enabled() {  // env TANQ_BLOCK_K2=1: standalone k = 2 ops through the block kernel too
+// standalone k = 2 ops whose targets sit at physical position >= 6 (the cooperative-tile
+// case) also run as one-sub-op blocks (2 group + 3 free qubits): QPE-16 132.1 vs 131.4
+// updates/s (profiles/r02_bench_c4_k2blk.json).  Env TANQ_BLOCK_K2=0 restores the tile kernel.
+bool block_k2_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("TANQ_BLOCK_K2");
-    on = (e && e[0] == '1') ? 1 : 0;
+    on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
 }

@@ -27,6 +27,6 @@ for tool in $TOOLS; do
     TANQ_BLOCK=$BLK TANQ_BLOCK_TMA=$TMA TANQ_GROUP=$1 TANQ_K2PATH=$2 TANQ_MIRROR=$3 TANQ_GRID_CAP=2 timeout 900 \
       /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 \
       python -c "$SNIP" > /tmp/san.$$ 2>&1
-    grep -E 'Race reported|Error|Invalid|SUMMARY|^ran' /tmp/san.$$ | sed -E 's/\+0x[0-9a-f]+//' | sort | uniq -c | head -20
+    grep -E 'Race reported|access at|Error|Invalid|SUMMARY|^ran' /tmp/san.$$ | sed -E 's/\+0x[0-9a-f]+//' | sort | uniq -c | head -20
   done
 done

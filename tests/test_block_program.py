@@ -87,8 +87,9 @@ def _bank_degrees(prm, blob):
 
 
 def test_block_layout_bank_conflict_free(Plan):
-    """QPE groups (3 qubits, all above qubit 1): every B / D fragment quarter-warp hits 8
-    distinct banks."""
+    """QPE groups (3 qubits, all above qubit 1): in the rotation layout every B / D fragment
+    quarter-warp hits 8 distinct banks; the TMA layout is accepted within one extra 2-way
+    conflict of it (TANQ_BLOCK_TMA_SLACK=1), so at most 2 lanes share a bank there."""
     c, nm = W.config_workload(4, n=8)
     plan = Plan(None, c, nm, fuse=2, k_max=3)
     seen = 0
@@ -98,7 +99,7 @@ def test_block_layout_bank_conflict_free(Plan):
         prog = plan.block_program(i, packed=True)
         if prog is None:
             continue
-        assert _bank_degrees(*prog) == 1, (i, qs)
+        assert _bank_degrees(*prog) <= (2 if prog[0].tma else 1), (i, qs)
         seen += 1
     assert seen >= 3
 
@@ -136,8 +137,8 @@ print("OK", seen)
 
 
 def test_block_program_standalone_k2():
-    """TANQ_BLOCK_K2=1: standalone k=2 ops with a target at physical position >= 6 run as a
-    one-sub-op block program (2 group qubits + 3 free qubits per block)."""
+    """Standalone k=2 ops with a target at physical position >= 6 run as a one-sub-op block
+    program (2 group qubits + 3 free qubits per block; default, TANQ_BLOCK_K2=1)."""
     import os
     import subprocess
     import sys

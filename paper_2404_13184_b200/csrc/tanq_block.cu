@@ -564,6 +564,9 @@ __global__ void __launch_bounds__(384, 1)
   int s = 0;
   while (cur < nb) {
     double2* X = stage0 + s * 1024;
+    // this thread's cp.async copies of the block have landed (the mbarrier below covers the
+    // other threads'; the explicit wait also lets compute-sanitizer's racecheck see it)
+    asm volatile("cp.async.wait_all;" ::: "memory");
     mbar_wait(&mbar[pair * 2 + s], parity[s]);
     parity[s] ^= 1u;
     if (pt == 0 && !first) bulk_wait_read0();  // last iteration's TMA store has read its stage

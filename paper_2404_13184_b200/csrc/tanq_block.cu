@@ -191,6 +191,51 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
     const int e = (mt * 4 + j) * 2 + c;
     return (int)((od[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
   };
+  if constexpr (ACC == 2) {
+    // all four n-tiles at once in two phases: k1 for 8 independent (n-tile, m-tile) chains,
+    // then the Re/Im chains seeded from k1 (16 chains), re-reading the B fragments from
+    // shared memory instead of keeping 32 of them in registers
+    double k1[4][2][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) k1[u][mt][0] = k1[u][mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 xb = X[boff(ks, u)];
+        const double sx = xb.x + xb.y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) dmma(k1[u][mt][0], k1[u][mt][1], a1[mt][ks], sx);
+      }
+    double yr[4][2][2], yi[4][2][2];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 xb = X[boff(ks, u)];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          if (ks == 0) {
+            dmma_c(yr[u][mt][0], yr[u][mt][1], a2[mt][0], xb.y, k1[u][mt][0], k1[u][mt][1]);
+            dmma_c(yi[u][mt][0], yi[u][mt][1], a3[mt][0], xb.x, k1[u][mt][0], k1[u][mt][1]);
+          } else {
+            dmma(yr[u][mt][0], yr[u][mt][1], a2[mt][ks], xb.y);
+            dmma(yi[u][mt][0], yi[u][mt][1], a3[mt][ks], xb.x);
+          }
+        }
+      }
+    __syncwarp();  // every lane's B loads precede any lane's D stores
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          X[doff(mt, u, c)] = make_double2(yr[u][mt][c], yi[u][mt][c]);
+    return;
+  }
 #pragma unroll
   for (int n0 = 0; n0 < 4; n0 += UI) {
     double2 xb[UI][4];
@@ -480,7 +525,7 @@ __global__ void __launch_bounds__(384, 1)
 //   otherwise -- every pair thread issues 16 cp.async 16 B copies (16 lanes per 256 B piece)
 //   straight to each element's final slot (pieces read from the transposed position land
 //   already permuted), conjugates them after the wait, and stores them back with STG.
-template <int UI>
+template <int UI, int ACC>
 __global__ void __launch_bounds__(384, 1)
     block_kernel_tma(double2* __restrict__ a, const __grid_constant__ BlockParams p,
                      const __grid_constant__ CUtensorMap tmap) {
@@ -601,7 +646,7 @@ __global__ void __launch_bounds__(384, 1)
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2)
-          blk_sub_k2<UI, 0>(Xh, F, T, lane, trow, 64);
+          blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, 64);
         else
           blk_sub_k1(Xh, F, T, trow, 64);
         __syncwarp();
@@ -674,9 +719,10 @@ static cudaError_t encode_block_tmap(CUtensorMap* map, double2* a, const BlockPa
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+template <int ACC>
 static cudaError_t launch_block_tma(double2* a, const BlockParams& p, cudaStream_t st) {
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = block_kernel_tma<2>;
+  auto kern = block_kernel_tma<2, ACC>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -742,14 +788,14 @@ size_t block_smem_bytes(int pairs, int blob_bytes) {
 // accumulators + 2 DADD per output instead of the seeded chain.
 cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStream_t st) {
   (void)L;
-  if (p.tma) return launch_block_tma(a, p, st);
   static int copy = -1, acc = -1;
   if (copy < 0) {
     const char* e = getenv("TANQ_BLOCK_COPY");
     copy = !e ? 0 : (e[0] == 'l' ? 1 : (!strcmp(e, "bs") ? 2 : 0));
     const char* f = getenv("TANQ_BLOCK_ACC");
-    acc = (f && f[0] == '1') ? 1 : 0;
+    acc = (f && f[0] == '1') ? 1 : ((f && f[0] == '2') ? 2 : 0);
   }
+  if (p.tma) return acc == 2 ? launch_block_tma<2>(a, p, st) : launch_block_tma<0>(a, p, st);
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
   if (acc == 1) {
@@ -757,6 +803,7 @@ cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStre
     if (copy == 2) return launch_block_cfg<2, 2, 1>(a, p, smem, st);
     return launch_block_cfg<2, 0, 1>(a, p, smem, st);
   }
+  if (acc == 2) return launch_block_cfg<2, 0, 2>(a, p, smem, st);
   if (copy == 1) return launch_block_cfg<2, 1, 0>(a, p, smem, st);
   if (copy == 2) return launch_block_cfg<2, 2, 0>(a, p, smem, st);
   return launch_block_cfg<2, 0, 0>(a, p, smem, st);

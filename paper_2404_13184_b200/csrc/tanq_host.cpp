@@ -331,6 +331,22 @@ FusedOp merge(const FusedOp& Q, const FusedOp& G) {
 // mode 1: paper -- merge into the latest op touching the same qubits only if it
 // acts on the identical ordered qubit tuple.  mode 2: greedy union up to k_max (<= 2 first,
 // then 3-qubit groups kept only when the cost model says they save passes).
+// 4-qubit groups (k_max = 4) run on the block kernel when they contain qubit 0 or 1 (a block
+// is the group + the lowest free qubit, and its lowest 4 bits must be qubits 0 and 1 for
+// 256 B contiguous pieces); other 4-qubit unions stay 3-qubit groups.  Env TANQ_QUAD_ANY=1
+// allows any 4-qubit group (round-1 behaviour: those run on the cooperative tile kernel).
+bool quad_ok(const int* q) {
+  static int any = -1;
+  if (any < 0) {
+    const char* e = std::getenv("TANQ_QUAD_ANY");
+    any = e && e[0] == '1' ? 1 : 0;
+  }
+  if (any) return true;
+  for (int i = 0; i < 4; ++i)
+    if (q[i] == 0 || q[i] == 1) return true;
+  return false;
+}
+
 std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   if (mode == 0) return in;
   auto pass = [&](const std::vector<FusedOp>& src, int klim, bool paper) {
@@ -406,6 +422,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
         }
       }
       if (uk > lim) fits = false;  // a dense k=3 op never joins a 4-qubit group
+      if (fits && uk == 4 && !quad_ok(uq)) fits = false;
       if (fits) {
         Q.op.k = uk;
         for (int i = 0; i < uk; ++i) Q.op.q[i] = uq[i];
@@ -447,7 +464,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
         for (int u = 0; u < uk; ++u) f |= uq[u] == A.op.q[t];
         if (!f) uq[uk++] = A.op.q[t];
       }
-      if (uk <= lim && uk >= 3) {  // (k <= 2 unions were already merged by level 1)
+      if (uk <= lim && uk >= 3 && (uk < 4 || quad_ok(uq))) {  // (k <= 2 unions: level 1)
         B.op.k = uk;
         for (int t = 0; t < uk; ++t) B.op.q[t] = uq[t];
         B.members.insert(B.members.begin(), A.members.begin(), A.members.end());
@@ -1171,7 +1188,18 @@ bool block_k2_enabled() {
 bool block_ok(const tanq_sim* s, const FusedOp& op) {
   if (!block_enabled() || s->L < 12) return false;
   if (op.k == 2 && op.sub.empty()) return block_k2_enabled() && k2_tiled(s, op);
-  if (op.k != 3 || op.sub.empty()) return false;
+  if (op.k == 4) {  // 4-qubit groups: the block's lowest 4 bits must be physical 0..3
+    if (op.sub.empty()) return false;
+    std::vector<int> pos;
+    for (int j = 0; j < 4; ++j)
+      for (int b = 0; b < 2; ++b) pos.push_back((int)s->phys[2 * op.q[j] + b]);
+    for (int f = 0; pos.size() < 10; ++f)
+      if (std::find(pos.begin(), pos.end(), f) == pos.end()) pos.push_back(f);
+    for (int b = 0; b < 4; ++b)
+      if (std::find(pos.begin(), pos.end(), b) == pos.end()) return false;
+  } else if (op.k != 3 || op.sub.empty()) {
+    return false;
+  }
   if ((int)op.sub.size() > tanq::kBlockMaxSub) return false;
   for (const auto& sb : op.sub)
     if (sb.k > 2) return false;

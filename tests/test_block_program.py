@@ -163,3 +163,32 @@ def test_block_program_tma_layout_forced():
                         "emulation_matches_oracle or standalone_k2"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("packed", [True, False])
+def test_block_program_four_qubit_groups(Plan, packed):
+    """k_max = 4: 4-qubit groups containing qubit 0 or 1 run as blocks (the group + the
+    lowest free qubit); their host programs must replay to the oracle's result."""
+    rng = np.random.default_rng(41 + packed)
+    seen = 0
+    for n, cfg in ((7, 3), (7, 4)):
+        c, nm = W.config_workload(cfg, n=n, depth=4) if cfg == 3 else W.config_workload(cfg, n=n)
+        plan = Plan(None, c, nm, fuse=2, k_max=4)
+        N = 2 ** n
+        for i, (qs, S) in enumerate(plan.ops()):
+            if len(qs) != 4:
+                continue
+            prog = plan.block_program(i, packed=packed)
+            assert prog is not None, qs                      # every 4-qubit group has 0 or 1
+            rho = (W.random_density(rng, n, rank=3) if packed
+                   else W.random_complex(rng, (N, N)) * 0.1)
+            a, _, _ = phys_of_rho(rho, n)
+            emulate(a, *prog)
+            ref = np.ascontiguousarray(rho.copy())
+            dense.apply_superop(ref, n, qs, S)
+            aref, _, _ = phys_of_rho(ref, n)
+            keep = (np.array([p <= pair_swap(int(p)) for p in range(N * N)]) if packed
+                    else np.ones(N * N, bool))
+            assert np.abs(a[keep] - aref[keep]).max() < 1e-12, (cfg, qs)
+            seen += 1
+    assert seen >= 2

@@ -183,6 +183,17 @@ typedef struct {
  * and 2n - log2(n_shards) >= 2 (ops on k qubits need 2k local bits).  Errors: TANQ_E_ARG, TANQ_E_NOMEM, TANQ_E_CUDA. */
 tanq_status tanq_create(int n_qubits, int n_shards, tanq_sim** out);
 
+/* Like tanq_create, with every shard in a caller-owned device buffer (e.g. a PyTorch tensor;
+ * SURVEY §8(b) tanq_create_ex): shard s in buffers[s] on device devices[s], each at least
+ * 16 * 4^n / n_shards bytes and 16-byte aligned.  The handle initialises the buffers to
+ * |0..0><0..0| and never frees them; the caller keeps them alive until tanq_destroy.  They
+ * hold vec(rho) in the library's physical layout (tanq_info_get reports the bit
+ * map); in the packed Hermitian layout only the canonical element of each transpose pair is
+ * current until tanq_get_state (which unpacks).  Errors: TANQ_E_ARG (size, alignment, not
+ * device memory of that device), TANQ_E_NOMEM (scratch), TANQ_E_CUDA. */
+tanq_status tanq_create_ex(int n_qubits, int n_shards, void* const* buffers, const int* devices,
+                           size_t bytes_each, tanq_sim** out);
+
 /* Multi-process mode (one process per GPU, launched by torchrun): this process holds shard
  * `rank` of `world_size` on `device`; remaps use NCCL point-to-point over NVLink.
  * nccl_uid: NCCL_UNIQUE_ID_BYTES (128) bytes from tanq_nccl_unique_id on rank 0, shared

@@ -540,6 +540,7 @@ struct Shard {
   int device = 0;
   cudaStream_t stream = nullptr;
   double2* data = nullptr;
+  bool external = false;  // caller-owned buffer (tanq_create_ex): never freed here
 };
 
 struct DevScratch {
@@ -2044,7 +2045,7 @@ static tanq_status create_common(int n, tanq_sim* s) {
     size_t fr = 0, tot = 0;
     CUDA_TRY(cudaMemGetInfo(&fr, &tot));
     int same = 0;
-    for (auto& o : s->shards) same += (o.device == sh.device && o.data == nullptr);
+    for (auto& o : s->shards) same += (o.device == sh.device && o.data == nullptr && !o.external);
     const size_t need = shard_bytes * (size_t)same + ((size_t)64 << 20) +
                         (s->dist ? 4 * s->xchunk * sizeof(double2) : 0) + (sizeof(double) * 3 << n);
     if (need > fr)
@@ -2058,7 +2059,7 @@ static tanq_status create_common(int n, tanq_sim* s) {
       CUDA_TRY(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
       s->owned.push_back({sh.device, sh.stream});
     }
-    CUDA_TRY(cudaMalloc(&sh.data, shard_bytes));
+    if (!sh.external) CUDA_TRY(cudaMalloc(&sh.data, shard_bytes));
     CUDA_TRY(tanq::launch_init(sh.data, (uint64_t)1 << s->L, sh.id == 0, sh.stream));
     s->launches++;
   }
@@ -2107,6 +2108,55 @@ tanq_status tanq_create(int n_qubits, int n_shards, tanq_sim** out) {
     Shard sh;
     sh.id = g;
     sh.device = g % ndev;
+    s->shards.push_back(sh);
+  }
+  tanq_status st = create_common(n_qubits, s);
+  if (st != TANQ_OK) {
+    tanq_destroy(s);
+    return st;
+  }
+  *out = s;
+  return TANQ_OK;
+}
+
+tanq_status tanq_create_ex(int n_qubits, int n_shards, void* const* buffers, const int* devices,
+                           size_t bytes_each, tanq_sim** out) {
+  if (!out || !buffers || !devices) return fail(TANQ_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 24) return fail(TANQ_E_ARG, "n_qubits must be in [1, 24]");
+  if (n_shards != 1 && n_shards != 2 && n_shards != 4 && n_shards != 8)
+    return fail(TANQ_E_ARG, "n_shards must be 1, 2, 4 or 8");
+  const int L = 2 * n_qubits - ilog2(n_shards);
+  if (L < 2) return fail(TANQ_E_ARG, "too few local bits for this shard count");
+  if (bytes_each < (sizeof(double2) << L))
+    return fail(TANQ_E_ARG, "buffer smaller than 16 * 4^n / n_shards bytes");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(TANQ_E_UNSUPPORTED, "no CUDA device");
+  }
+  for (int g = 0; g < n_shards; ++g) {
+    if (!buffers[g] || (reinterpret_cast<uintptr_t>(buffers[g]) & 15))
+      return fail(TANQ_E_ARG, "shard buffer NULL or not 16-byte aligned");
+    if (devices[g] < 0 || devices[g] >= ndev) return fail(TANQ_E_ARG, "bad device");
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, buffers[g]) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+        pa.device != devices[g]) {
+      cudaGetLastError();
+      return fail(TANQ_E_ARG, "shard buffer is not device memory of the given device");
+    }
+  }
+  tanq_sim* s = new tanq_sim();
+  s->n = n_qubits;
+  s->L = L;
+  s->world = n_shards;
+  s->rank0 = 0;
+  for (int g = 0; g < n_shards; ++g) {
+    Shard sh;
+    sh.id = g;
+    sh.device = devices[g];
+    sh.data = static_cast<double2*>(buffers[g]);
+    sh.external = true;
     s->shards.push_back(sh);
   }
   tanq_status st = create_common(n_qubits, s);
@@ -2203,7 +2253,7 @@ tanq_status tanq_destroy(tanq_sim* s) {
   for (auto& sh : s->shards) {
     cudaSetDevice(sh.device);
     if (sh.stream) cudaStreamSynchronize(sh.stream);
-    if (sh.data) cudaFree(sh.data);
+    if (sh.data && !sh.external) cudaFree(sh.data);
   }
   for (auto& p : s->owned) {
     cudaSetDevice(p.first);

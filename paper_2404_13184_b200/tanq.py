@@ -113,6 +113,8 @@ _P, _I, _U64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_doub
 SIGNATURES = {
     "tanq_create": ([_I, _I, ctypes.POINTER(_P)], _I),
     "tanq_create_dist": ([_I, _I, _I, _I, _P, ctypes.POINTER(_P)], _I),
+    "tanq_create_ex": ([_I, _I, ctypes.POINTER(_P), ctypes.POINTER(_I), ctypes.c_size_t,
+                        ctypes.POINTER(_P)], _I),
     "tanq_nccl_unique_id": ([_P, ctypes.c_size_t], _I),
     "tanq_destroy": ([_P], _I),
     "tanq_reset": ([_P], _I),
@@ -450,10 +452,20 @@ class Simulator:
     """One handle of libtanq (tanq_create / tanq_create_dist)."""
 
     def __init__(self, n_qubits: int, n_shards: int = 1, *, world_size: int = 0, rank: int = 0,
-                 device: int = 0, nccl_uid: Optional[bytes] = None):
+                 device: int = 0, nccl_uid: Optional[bytes] = None, buffers=None):
         self.n = n_qubits
         h = ctypes.c_void_p()
-        if world_size:
+        if buffers is not None:
+            # caller-owned device buffers (tanq_create_ex), e.g. torch tensors: anything with
+            # data_ptr(), nbytes and a .device.index; kept referenced for the handle's lifetime
+            self._buffers = list(buffers)
+            ptrs = (ctypes.c_void_p * len(self._buffers))(*[b.data_ptr() for b in self._buffers])
+            devs = (ctypes.c_int * len(self._buffers))(*[int(b.device.index or 0)
+                                                         for b in self._buffers])
+            nbytes = min(int(b.nbytes) for b in self._buffers)
+            _check(lib().tanq_create_ex(n_qubits, len(self._buffers), ptrs, devs, nbytes,
+                                        ctypes.byref(h)), "tanq_create_ex")
+        elif world_size:
             uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid else None
             _check(lib().tanq_create_dist(n_qubits, world_size, rank, device, uid,
                                           ctypes.byref(h)), "tanq_create_dist")

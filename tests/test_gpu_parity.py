@@ -488,3 +488,30 @@ def test_run_circuit_plan_cache(Sim):
         sim.reset()
         sim.run_circuit(c, nm)
         assert_parity(rho_of(sim, n), ref3)
+
+
+def test_create_ex_on_torch_buffer(Sim):
+    """tanq_create_ex: the state lives in a caller-owned torch tensor; after
+    get_state (which unpacks) the tensor holds vec(rho) in the physical interleaved layout:
+    element (r, c) at sum_q r_q 2^(2q) + c_q 2^(2q+1)."""
+    import torch
+    n = 6
+    N = 2 ** n
+    c = W.random_circuit(n, 40, seed=606, kmax=3)
+    nm = W.synthetic_calibration(c, 606, depol=True, thermal=True, overrot=True)
+    ref = dense.run(c, nm)
+    buf = torch.empty(4 ** n, dtype=torch.complex128, device="cuda")
+    with Sim(n, buffers=[buf]) as sim:
+        torch.cuda.synchronize()
+        assert abs(buf[0].item() - 1) == 0 and torch.count_nonzero(buf).item() == 1
+        sim.run_circuit(c, nm)
+        got = rho_of(sim, n)
+        assert_parity(got, ref)
+        sim.sync()
+        raw = buf.cpu().numpy()
+    r = np.arange(N)
+    P_r = np.zeros(N, dtype=np.int64)
+    for q in range(n):
+        P_r |= ((r >> q) & 1) << (2 * q)
+    phys = P_r[:, None] | (P_r[None, :] << 1)           # [row, col] -> physical index
+    assert np.abs(raw[phys] - ref).max() <= 1e-10

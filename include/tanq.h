@@ -34,6 +34,12 @@
  * 2n index bits of vec(rho) are permuted so that the row and column bits of
  * each qubit are adjacent (rowpos(q)=2q, colpos(q)=2q+1 initially) and the
  * top log2(n_shards) bits select the shard (P:161 partitions by high bits).
+ * With several shards the default is the shard-local parity layout
+ * (DESIGN.md §7): the g = log2(world) top qubits are half-global -- the
+ * shard bit holds row XOR col of the qubit (invariant under transpose, so a
+ * transpose pair never leaves its shard and the packed Hermitian layout
+ * runs on every shard), the row bit is local; env TANQ_LAYOUT=bits selects
+ * the plain bit layout.
  */
 #ifndef TANQ_ABI_H_
 #define TANQ_ABI_H_
@@ -159,8 +165,10 @@ typedef struct {
   int32_t rank;            /* first shard id held by this process */
   int32_t local_bits;      /* log2(amplitudes per shard) */
   int32_t rowpos[32];      /* current physical bit of qubit q's row bit */
-  int32_t colpos[32];
+  int32_t colpos[32];      /* (parity layout: for a half-global qubit, the global bit that
+                              holds row XOR col) */
   uint64_t shard_bytes;
+  uint64_t parity_qubits;  /* half-global qubits of the shard-local parity layout (bit q) */
 } tanq_info;
 
 /* Per-kernel-class timing accumulated while flags bit0 is set (CUDA events on the

@@ -48,6 +48,11 @@ namespace {
 __device__ __forceinline__ uint64_t pair_swap64(uint64_t x) {
   return ((x & 0x5555555555555555ull) << 1) | ((x >> 1) & 0x5555555555555555ull);
 }
+// transpose of an index with r low bits removed under the shard's descriptor (TDesc)
+__device__ __forceinline__ uint64_t tpose64(uint64_t x, uint64_t lo, uint64_t m, int r) {
+  const uint64_t l = lo >> r;
+  return pair_swap64(x & l) | ((x & ~l) ^ (m >> r));
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -394,18 +399,20 @@ __global__ void __launch_bounds__(384, 1)
   const bool mirror = p.mirror != 0;
   auto next_block = [&](uint64_t i) {
     if (mirror)
-      while (i < nb && i > pair_swap64(i)) i += npairs;
+      while (i < nb && i > tpose64(i, p.tp_lo, p.tp_m, 10)) i += npairs;
     return i;
   };
   // where piece (offset go) of the block at `base` lives: in place, or (packed layout,
   // non-canonical piece of a block that is not self-transposed) at the transposed position
   auto piece_src = [&](uint64_t base, bool self, uint64_t go, bool& tr) {
     const uint64_t e0 = base + go;
-    const uint64_t em = pair_swap64(e0);
+    const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
     tr = mirror && !self && e0 > em;
     return tr ? em : e0;
   };
-  auto is_self = [&](uint64_t base) { return mirror && pair_swap64(base) == base; };
+  auto is_self = [&](uint64_t base) {
+    return mirror && tpose64(base, p.tp_lo, p.tp_m, 0) == base;
+  };
   auto issue = [&](uint64_t i, int s) {
     uint64_t* bar = &mbar[pair * 2 + s];
     double2* st = stage0 + s * kStageUnits;
@@ -552,13 +559,14 @@ __global__ void __launch_bounds__(384, 1)
   const bool mirror = p.mirror != 0;
   auto next_block = [&](uint64_t i) {
     if (mirror)
-      while (i < nb && i > pair_swap64(i)) i += npairs;
+      while (i < nb && i > tpose64(i, p.tp_lo, p.tp_m, 10)) i += npairs;
     return i;
   };
   // block classification: 0 direct (TMA), 1 cp.async with transposed pieces, 2 self-transposed
   auto kind_of = [&](uint64_t base) {
     if (!mirror) return 0;
-    const uint64_t d = (base ^ (base >> 1)) & 0x5555555555555555ull;
+    const uint64_t d =
+        (base ^ tpose64(base, p.tp_lo, p.tp_m, 0)) & (0x5555555555555555ull | ~p.tp_lo);
     if (!d) return 2;
     return (63 - __clzll(d)) > p.hi_blk ? 0 : 1;
   };
@@ -592,7 +600,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int it = 0; it < 16; ++it) {
         const int q = it * 4 + qb;
         const uint64_t e0 = base + p.piece_goff[q];
-        const uint64_t em = pair_swap64(e0);
+        const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
         const bool tr = kd == 1 && e0 > em;
         cp_async16_cg(st + sSlot[q * 16 + (tr ? pswap4(u) : u)], a + (tr ? em : e0) + u);
       }
@@ -619,7 +627,7 @@ __global__ void __launch_bounds__(384, 1)
     const int kd = (p.dbg & 2) ? 0 : kind_of(base);
     if (kd == 1) {  // conjugate the pieces that came from the transposed position
       const uint64_t e0 = base + p.piece_goff[pt];
-      if (e0 > pair_swap64(e0)) {
+      if (e0 > tpose64(e0, p.tp_lo, p.tp_m, 0)) {
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           double* im = &X[sSlot[pt * 16 + ((t + pt) & 15)]].y;
@@ -668,7 +676,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int it = 0; it < 16; ++it) {
           const int q = it * 4 + qb;
           const uint64_t e0 = base + p.piece_goff[q];
-          const uint64_t em = pair_swap64(e0);
+          const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
           const bool tr = kd == 1 && e0 > em;
           double2 v = X[sSlot[q * 16 + (tr ? pswap4(u) : u)]];
           if (tr) v.y = -v.y;

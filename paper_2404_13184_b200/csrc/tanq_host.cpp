@@ -571,6 +571,9 @@ struct tanq_sim {
   std::vector<Shard> shards;
   std::vector<DevScratch> scratch;  // per distinct device
   uint32_t phys[64];                // logical bit (2q row, 2q+1 col) -> physical bit
+  uint64_t par = 0;                 // parity layout: half-global qubits (phys[2h+1] is a global
+                                    // bit holding r_h XOR c_h, phys[2h] the local row bit)
+  bool parity = false;              // shard-local parity layout, world > 1
   ncclComm_t comm = nullptr;
   double2* xsend = nullptr;         // 2 staging slots of xchunk elements (send)
   double2* xrecv = nullptr;         // 2 staging slots (receive)
@@ -630,15 +633,69 @@ tanq_status ensure_scratch(tanq_sim* s, DevScratch& d) {
   return TANQ_OK;
 }
 
+int ilog2_(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
 tanq::BitMap bitmap_of(const tanq_sim* s) {
   tanq::BitMap bm;
   bm.nbits = 2 * s->n;
   for (int i = 0; i < 64; ++i) bm.phys[i] = s->phys[i];
+  bm.par = s->par;
   return bm;
 }
 
+// Multi-shard layout.  env TANQ_LAYOUT=bits: the round-1 layout (identity bit
+// map, the top log2 G physical bits -- row / col bits of the top qubits -- select the shard,
+// transpose pairs cross shards, so multi-shard runs cannot use the packed Hermitian layout).
+// Default: the shard-local parity layout -- the top g = log2 G qubits are half-global: qubit
+// h's global bit holds r_h XOR c_h (invariant under transpose, so every transpose pair stays
+// on its shard) and its row bit is local, above the aligned (row, col) pairs of the n - g
+// fully local qubits.
+// It needs n - g >= 5 fully local qubits (a 4-qubit op on a half-global qubit still finds a
+// victim); smaller registers keep the bit layout.
+bool parity_layout_for(int n, int world) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TANQ_LAYOUT");
+    v = e && !std::strcmp(e, "bits") ? 0 : 1;
+  }
+  int g = 0;
+  while ((1 << g) < world) ++g;
+  return v == 1 && world > 1 && n - g >= 5;
+}
+
+void init_layout(uint32_t* phys, uint64_t& par, int n, int g, bool parity) {
+  for (int i = 0; i < 64; ++i) phys[i] = (uint32_t)i;  // rowpos(q)=2q, colpos(q)=2q+1
+  par = 0;
+  if (!parity || g == 0) return;
+  const int F = n - g, L = 2 * n - g;
+  for (int i = 0; i < g; ++i) {
+    const int h = F + i;
+    phys[2 * h] = (uint32_t)(2 * F + i);  // local row bit above the pairs
+    phys[2 * h + 1] = (uint32_t)(L + i);  // global parity bit
+    par |= 1ull << h;
+  }
+}
+
 void reset_layout(tanq_sim* s) {
-  for (int i = 0; i < 64; ++i) s->phys[i] = (uint32_t)i;  // rowpos(q)=2q, colpos(q)=2q+1
+  init_layout(s->phys, s->par, s->n, ilog2_(s->world), s->parity);
+}
+
+// Transpose descriptor of shard `id` (tanq::TDesc): pairs below 2 (n - g) in the parity
+// layout; the half-global row bits flip where the shard's parity bit is 1.
+tanq::TDesc tdesc_of(const tanq_sim* s, int id) {
+  tanq::TDesc td;
+  if (!s->par) return td;
+  const int g = __builtin_popcountll(s->par);
+  td.lo = ((uint64_t)1 << (2 * (s->n - g))) - 1;
+  for (uint64_t h = s->par; h; h &= h - 1) {
+    const int q = __builtin_ctzll(h);
+    if ((id >> (s->phys[2 * q + 1] - s->L)) & 1) td.m |= (uint64_t)1 << s->phys[2 * q];
+  }
+  return td;
 }
 
 tanq_status host_wait(tanq_sim* s, cudaStream_t st);
@@ -898,6 +955,59 @@ tanq_status remap_swap2(tanq_sim* s, int a0, int b0, int a1, int b1) {
   return TANQ_OK;
 }
 
+void apply_parity_remap(uint32_t* phys, uint64_t& par, int h, int v);
+
+// Parity-layout remap: half-global qubit h becomes fully local in the pair of
+// the fully local qubit v, which becomes half-global.  Half of every shard crosses to the
+// partner shard (the one differing in h's global bit); a quarter moves inside the shard.
+tanq_status remap_parity(tanq_sim* s, int h, int v) {
+  TRY(ensure_unpacked(s));
+  const int L = s->L;
+  const int x = (int)s->phys[2 * h], a = (int)s->phys[2 * h + 1];
+  const int y = (int)s->phys[2 * v], z = (int)s->phys[2 * v + 1], gb = a - L;
+  const uint64_t half = (uint64_t)1 << (L - 1);
+  if (!s->dist) {
+    for (auto& sh : s->shards) {
+      const int g = sh.id;
+      if ((g >> gb) & 1) continue;
+      const int g2 = g ^ (1 << gb);
+      Shard* other = nullptr;
+      for (auto& o : s->shards)
+        if (o.id == g2) other = &o;
+      TRY(stream_wait(sh, *other));
+      CUDA_TRY(cudaSetDevice(sh.device));
+      // both shards read once, 3/4 of them written
+      Prof pr{3, nullptr, nullptr, 3.5 * (double)((uint64_t)1 << L) * sizeof(double2), 0.0, 0.0};
+      prof_begin(s, sh, pr);
+      CUDA_TRY(tanq::launch_parity_swap(sh.data, other->data, L, x, y, z, sh.stream));
+      prof_end(s, sh, pr);
+      s->launches++;
+      TRY(stream_wait(*other, sh));
+      s->remap_bytes += half * sizeof(double2);
+    }
+  } else {
+    Shard& sh = s->shards[0];
+    const int g = sh.id, g2 = g ^ (1 << gb), sa = (g >> gb) & 1;
+    CUDA_TRY(cudaSetDevice(sh.device));
+    Prof pr{3, nullptr, nullptr, 2.0 * half * sizeof(double2), 0.0, 0.0};
+    prof_begin(s, sh, pr);
+    CUDA_TRY(tanq::launch_parity_stay(sh.data, L, x, y, z, sa, sh.stream));
+    s->launches++;
+    TRY(exchange_pipelined(
+        s, sh, g2, half,
+        [&](uint64_t first, uint64_t cnt, double2* buf) {
+          return tanq::launch_parity_pack(sh.data, buf, L, x, y, z, sa, first, cnt, sh.stream);
+        },
+        [&](uint64_t first, uint64_t cnt, const double2* buf) {
+          return tanq::launch_parity_unpack(sh.data, buf, L, x, y, z, sa, first, cnt, sh.stream);
+        }));
+    prof_end(s, sh, pr);
+  }
+  apply_parity_remap(s->phys, s->par, h, v);
+  s->remap_count++;
+  return TANQ_OK;
+}
+
 // Victim for a remap (pure layout logic, shared by execution and tanq_plan_schedule): a local
 // bit not targeted by the op whose qubit is used furthest in the future (lookahead 256 ops
 // over `next` from `next_from`), ties to the highest position.  -1 if none.
@@ -931,10 +1041,71 @@ int choose_victim(const uint32_t* phys, int n, int L, const std::vector<int>& tg
   return best;
 }
 
-// The remaps (a global, b local) that make op `op` local, applied to `phys` in order.
-std::vector<std::pair<int, int>> plan_remaps(uint32_t* phys, int n, int L, const FusedOp& op,
-                                             const std::vector<FusedOp>* next, size_t next_from) {
-  std::vector<std::pair<int, int>> out;
+// A remap step.  kind 1 (bit layout): swap global bit a with local bit b.  kind 2 (parity
+// layout): half-global qubit a and fully local qubit b trade places.
+struct Remap {
+  int kind, a, b;
+};
+
+// Parity-layout victim: a fully local qubit the op does not target whose next use is furthest
+// (lookahead 256 ops), ties to the highest pair.  -1 if none.
+int choose_victim_qubit(const uint32_t* phys, uint64_t par, int n, const FusedOp& op,
+                        const std::vector<FusedOp>* next, size_t next_from) {
+  int best = -1;
+  long best_dist = -1;
+  uint32_t best_pos = 0;
+  for (int q = 0; q < n; ++q) {
+    if ((par >> q) & 1) continue;
+    bool tgt = false;
+    for (int j = 0; j < op.k; ++j) tgt |= op.q[j] == q;
+    if (tgt) continue;
+    long dist = 1L << 40;
+    if (next) {
+      for (size_t t = next_from; t < next->size() && t < next_from + 256; ++t) {
+        const FusedOp& f = (*next)[t];
+        bool uses = false;
+        for (int j = 0; j < f.k; ++j) uses |= f.q[j] == q;
+        if (uses) {
+          dist = (long)(t - next_from);
+          break;
+        }
+      }
+    }
+    if (dist > best_dist || (dist == best_dist && phys[2 * q] > best_pos)) {
+      best_dist = dist;
+      best = q;
+      best_pos = phys[2 * q];
+    }
+  }
+  return best;
+}
+
+// Bookkeeping of a parity remap: qubit h takes v's (row, col) pair, v's row bit goes to h's
+// local row slot and its parity to h's global bit.
+void apply_parity_remap(uint32_t* phys, uint64_t& par, int h, int v) {
+  const uint32_t x = phys[2 * h], a = phys[2 * h + 1], y = phys[2 * v], z = phys[2 * v + 1];
+  phys[2 * h] = y;
+  phys[2 * h + 1] = z;
+  phys[2 * v] = x;
+  phys[2 * v + 1] = a;
+  par ^= ((uint64_t)1 << h) | ((uint64_t)1 << v);
+}
+
+// The remaps that make op `op` local, applied to (phys, par) in order ({-1, ..} on failure).
+std::vector<Remap> plan_remaps(uint32_t* phys, uint64_t& par, int n, int L, const FusedOp& op,
+                               const std::vector<FusedOp>* next, size_t next_from) {
+  std::vector<Remap> out;
+  if (par) {
+    for (int j = 0; j < op.k; ++j) {
+      const int h = op.q[j];
+      if (!((par >> h) & 1)) continue;
+      const int v = choose_victim_qubit(phys, par, n, op, next, next_from);
+      if (v < 0) return {{-1, -1, -1}};
+      out.push_back({2, h, v});
+      apply_parity_remap(phys, par, h, v);
+    }
+    return out;
+  }
   std::vector<int> tgt;
   for (int j = 0; j < op.k; ++j) {
     tgt.push_back(2 * op.q[j]);
@@ -944,8 +1115,8 @@ std::vector<std::pair<int, int>> plan_remaps(uint32_t* phys, int n, int L, const
     const int a = (int)phys[id];
     if (a < L) continue;
     const int b = choose_victim(phys, n, L, tgt, next, next_from);
-    if (b < 0) return {{-1, -1}};
-    out.push_back({a, b});
+    if (b < 0) return {{-1, -1, -1}};
+    out.push_back({1, a, b});
     for (int i = 0; i < 2 * n; ++i) {
       if (phys[i] == (uint32_t)a)
         phys[i] = (uint32_t)b;
@@ -961,15 +1132,20 @@ tanq_status ensure_local(tanq_sim* s, const FusedOp& op, const std::vector<Fused
                          size_t next_from) {
   uint32_t phys[64];
   std::memcpy(phys, s->phys, sizeof(phys));
-  auto swaps = plan_remaps(phys, s->n, s->L, op, next, next_from);
-  for (auto& ab : swaps)
-    if (ab.first < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
+  uint64_t par = s->par;
+  auto swaps = plan_remaps(phys, par, s->n, s->L, op, next, next_from);
+  for (auto& r : swaps)
+    if (r.kind < 0) return fail(TANQ_E_ARG, "no local qubit available for remap");
+  if (s->par) {
+    for (auto& r : swaps) TRY(remap_parity(s, r.a, r.b));
+    return TANQ_OK;
+  }
   // swaps are independent (distinct global and distinct local bits): batch them in pairs
   size_t i = 0;
   if (s->dist && batch_remaps())
     for (; i + 1 < swaps.size(); i += 2)
-      TRY(remap_swap2(s, swaps[i].first, swaps[i].second, swaps[i + 1].first, swaps[i + 1].second));
-  for (; i < swaps.size(); ++i) TRY(remap_swap(s, swaps[i].first, swaps[i].second));
+      TRY(remap_swap2(s, swaps[i].a, swaps[i].b, swaps[i + 1].a, swaps[i + 1].b));
+  for (; i < swaps.size(); ++i) TRY(remap_swap(s, swaps[i].a, swaps[i].b));
   return TANQ_OK;
 }
 
@@ -1030,11 +1206,18 @@ std::vector<double2> member_order_S(const FusedOp& op, const MemberMap& mm) {
 // Packed Hermitian mode: rho known Hermitian, op Hermiticity-preserving, one
 // shard with the initial interleaved layout (row/col bits of every qubit adjacent, so the
 // transpose of element e is pair_swap(e)), whole 16-tuple blocks.
+// Several shards: the shard-local parity layout, whose transpose pairs never
+// leave their shard; every kernel's in-tile bits (targets + lowest free qubits, at most 6
+// qubits) must lie below the pair boundary, so at least 6 fully local qubits.
 bool use_mirror(const tanq_sim* s, const FusedOp& op) {
-  if (!s->mirror_allowed || !s->herm_state || !op.herm || s->shards.size() != 1 || s->dist)
-    return false;
-  for (int i = 0; i < 2 * s->n; ++i)
-    if (s->phys[i] != (uint32_t)i) return false;
+  if (!s->mirror_allowed || !s->herm_state || !op.herm) return false;
+  if (s->par) {
+    if (s->n - __builtin_popcountll(s->par) < 6) return false;
+  } else {
+    if (s->shards.size() != 1 || s->dist) return false;
+    for (int i = 0; i < 2 * s->n; ++i)
+      if (s->phys[i] != (uint32_t)i) return false;
+  }
   const int tuple_bits = s->L - 2 * op.k;  // groups: op.k = tile qubits (3 or 4)
   return op.k == 1 ? tuple_bits >= 2 : tuple_bits >= 4;
 }
@@ -1084,6 +1267,11 @@ void build_group(const tanq_sim* s, const FusedOp& op, tanq::GroupParams& p, dou
   }
   p.n_tuples = (uint64_t)1 << (s->L - TBITS);
   p.mirror = use_mirror(s, op) ? 1u : 0u;
+  {
+    const tanq::TDesc td = tdesc_of(s, s->shards.empty() ? 0 : s->shards[0].id);
+    p.tp_lo = td.lo;
+    p.tp_m = td.m;
+  }
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = std::getenv("TANQ_DBG");
@@ -1473,7 +1661,8 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       // element is stored, i.e. the base differs at a qubit above the group -- require at least
       // two qubits above the group (about 3/4 of the processed blocks or more); the others go
       // through the cp.async path
-      const bool mostly_direct = !use_mirror(s, op) || bpos[9] + 4 < s->L;
+      const int pair_top = s->par ? 2 * (s->n - __builtin_popcountll(s->par)) : s->L;
+      const bool mostly_direct = !use_mirror(s, op) || bpos[9] + 4 < pair_top;
       static int slack = -1;
       if (slack < 0) {
         const char* e = std::getenv("TANQ_BLOCK_TMA_SLACK");
@@ -1530,6 +1719,11 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   for (int j = 0; j < 10; ++j) p.lo_mask[j] = ((uint64_t)1 << bpos[j]) - 1;
   p.n_blocks = (uint64_t)1 << (s->L - 10);
   p.mirror = use_mirror(s, op) ? 1u : 0u;
+  {
+    const tanq::TDesc td = tdesc_of(s, s->shards.empty() ? 0 : s->shards[0].id);
+    p.tp_lo = td.lo;
+    p.tp_m = td.m;
+  }
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = std::getenv("TANQ_DBG");
@@ -1657,13 +1851,14 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
 // layout does not keep up to date.
 tanq_status ensure_unpacked(tanq_sim* s) {
   if (!s->packed) return TANQ_OK;
-  Shard& sh = s->shards[0];
-  CUDA_TRY(cudaSetDevice(sh.device));
-  Prof pr{4, nullptr, nullptr, 16.0 * (double)((uint64_t)1 << s->L), 0.0, 0.0};
-  prof_begin(s, sh, pr);
-  CUDA_TRY(tanq::launch_unpack(sh.data, s->L, sh.stream));
-  prof_end(s, sh, pr);
-  s->launches++;
+  for (auto& sh : s->shards) {
+    CUDA_TRY(cudaSetDevice(sh.device));
+    Prof pr{4, nullptr, nullptr, 16.0 * (double)((uint64_t)1 << s->L), 0.0, 0.0};
+    prof_begin(s, sh, pr);
+    CUDA_TRY(tanq::launch_unpack(sh.data, s->L, tdesc_of(s, sh.id), sh.stream));
+    prof_end(s, sh, pr);
+    s->launches++;
+  }
   s->packed = false;
   return TANQ_OK;
 }
@@ -1703,6 +1898,7 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
     Prof pr{std::min(k, 3) - 1, nullptr, nullptr, (mir ? 16.0 : 32.0) * amps,
             fr * flops_amp * amps, fr * hw_amp * amps};
     prof_begin(s, sh, pr);
+    const tanq::TDesc td = tdesc_of(s, sh.id);
     if (gp || bp) {
       int di = 0;
       for (size_t i = 0; i < s->scratch.size(); ++i)
@@ -1710,6 +1906,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       if (bp) {
         tanq::BlockParams p = *bp;
         p.blob = (*prog)[di];
+        p.tp_lo = td.lo;
+        p.tp_m = td.m;
         g_err.clear();
         const cudaError_t be = tanq::launch_block_group(sh.data, p, s->L, sh.stream);
         if (be != cudaSuccess)
@@ -1718,6 +1916,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       } else {
         tanq::GroupParams p = *gp;
         p.prog = (*prog)[di];
+        p.tp_lo = td.lo;
+        p.tp_m = td.m;
         CUDA_TRY(tanq::launch_group3(sh.data, p, sh.stream));
       }
     } else if (k == 1) {
@@ -1729,6 +1929,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       }
       p.n_tuples = n_tuples;
       p.mirror = mir ? 1u : 0u;
+      p.tp_lo = td.lo;
+      p.tp_m = td.m;
       CUDA_TRY(tanq::launch_gate1(sh.data, p, sh.stream));
     } else if (k == 2) {
       tanq::GateParams<2> p;
@@ -1739,6 +1941,8 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
       }
       p.n_tuples = n_tuples;
       p.mirror = mir ? 1u : 0u;
+      p.tp_lo = td.lo;
+      p.tp_m = td.m;
       CUDA_TRY(tanq::launch_gate2(sh.data, p, sh.stream));
     } else {
       return fail(TANQ_E_UNSUPPORTED, "k >= 3 op without a group program");
@@ -2104,6 +2308,7 @@ tanq_status tanq_create(int n_qubits, int n_shards, tanq_sim** out) {
   s->L = L;
   s->world = n_shards;
   s->rank0 = 0;
+  s->parity = parity_layout_for(n_qubits, n_shards);
   for (int g = 0; g < n_shards; ++g) {
     Shard sh;
     sh.id = g;
@@ -2151,6 +2356,7 @@ tanq_status tanq_create_ex(int n_qubits, int n_shards, void* const* buffers, con
   s->L = L;
   s->world = n_shards;
   s->rank0 = 0;
+  s->parity = parity_layout_for(n_qubits, n_shards);
   for (int g = 0; g < n_shards; ++g) {
     Shard sh;
     sh.id = g;
@@ -2200,6 +2406,7 @@ tanq_status tanq_create_dist(int n_qubits, int world_size, int rank, int device,
   s->world = world_size;
   s->rank0 = rank;
   s->dist = true;
+  s->parity = parity_layout_for(n_qubits, world_size);
   Shard sh;
   sh.id = rank;
   sh.device = device;
@@ -2311,6 +2518,7 @@ tanq_status tanq_info_get(tanq_sim* s, tanq_info* o) {
     o->colpos[q] = (int)s->phys[2 * q + 1];
   }
   o->shard_bytes = sizeof(double2) << s->L;
+  o->parity_qubits = s->par;
   return TANQ_OK;
 }
 
@@ -2601,7 +2809,8 @@ tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* item
     return fail(TANQ_E_ARG, "world_size must be 1, 2, 4 or 8");
   const int L = 2 * p->n - ilog2(world_size);
   uint32_t phys[64];
-  for (int i = 0; i < 64; ++i) phys[i] = (uint32_t)i;
+  uint64_t par = 0;
+  init_layout(phys, par, p->n, ilog2(world_size), parity_layout_for(p->n, world_size));
   uint64_t cnt = 0;
   auto put = [&](int32_t a, int32_t b, int32_t c) {
     if (items && cnt < max) {
@@ -2613,9 +2822,9 @@ tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* item
   };
   for (size_t i = 0; i < p->ops.size(); ++i) {
     if (2 * p->ops[i].k > L) return fail(TANQ_E_ARG, "op needs more local bits than a shard holds");
-    for (auto& ab : plan_remaps(phys, p->n, L, p->ops[i], &p->ops, i + 1)) {
-      if (ab.first < 0) return fail(TANQ_E_ARG, "no local bit available for remap");
-      put(1, ab.first, ab.second);
+    for (auto& r : plan_remaps(phys, par, p->n, L, p->ops[i], &p->ops, i + 1)) {
+      if (r.kind < 0) return fail(TANQ_E_ARG, "no local qubit available for remap");
+      put(r.kind, r.a, r.b);
     }
     put(0, (int32_t)i, 0);
   }
@@ -3030,23 +3239,32 @@ tanq_status tanq_check_hermitian(tanq_sim* s, double tol, int* is_herm) {
     *is_herm = 1;
     return TANQ_OK;
   }
-  if (s->shards.size() != 1 || s->dist) return TANQ_OK;  // transpose pairs span shards
-  for (int i = 0; i < 2 * s->n; ++i)
-    if (s->phys[i] != (uint32_t)i) return TANQ_OK;
-  Shard& sh = s->shards[0];
-  DevScratch& d = scratch_for(s, sh.device);
-  TRY(ensure_scratch(s, d));
-  CUDA_TRY(cudaSetDevice(sh.device));
-  unsigned long long* res = reinterpret_cast<unsigned long long*>(d.scal);  // [diff, maxabs]
-  CUDA_TRY(cudaMemsetAsync(res, 0, 2 * sizeof(unsigned long long), sh.stream));
-  CUDA_TRY(tanq::launch_herm_check(sh.data, s->L, res, sh.stream));
-  s->launches++;
-  unsigned long long h[2];
-  CUDA_TRY(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, sh.stream));
-  TRY(host_wait(s, sh.stream));
-  double diff, mx;
-  std::memcpy(&diff, &h[0], sizeof(double));
-  std::memcpy(&mx, &h[1], sizeof(double));
+  // transpose pairs must stay on their shard: one shard in the identity layout, or the
+  // parity layout (single process; a multi-process handle would need a reduction)
+  if (s->dist && s->world > 1) return TANQ_OK;
+  if (!s->par) {
+    if (s->shards.size() != 1) return TANQ_OK;
+    for (int i = 0; i < 2 * s->n; ++i)
+      if (s->phys[i] != (uint32_t)i) return TANQ_OK;
+  }
+  double diff = 0.0, mx = 0.0;
+  for (auto& sh : s->shards) {
+    DevScratch& d = scratch_for(s, sh.device);
+    TRY(ensure_scratch(s, d));
+    CUDA_TRY(cudaSetDevice(sh.device));
+    unsigned long long* res = reinterpret_cast<unsigned long long*>(d.scal);  // [diff, maxabs]
+    CUDA_TRY(cudaMemsetAsync(res, 0, 2 * sizeof(unsigned long long), sh.stream));
+    CUDA_TRY(tanq::launch_herm_check(sh.data, s->L, tdesc_of(s, sh.id), res, sh.stream));
+    s->launches++;
+    unsigned long long h[2];
+    CUDA_TRY(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, sh.stream));
+    TRY(host_wait(s, sh.stream));
+    double dd, mm;
+    std::memcpy(&dd, &h[0], sizeof(double));
+    std::memcpy(&mm, &h[1], sizeof(double));
+    diff = std::max(diff, dd);
+    mx = std::max(mx, mm);
+  }
   *is_herm = diff <= tol * std::max(1.0, mx) ? 1 : 0;
   s->herm_state = *is_herm != 0;
   return TANQ_OK;

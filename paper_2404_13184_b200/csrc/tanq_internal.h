@@ -21,6 +21,7 @@ struct GateParams {
   uint64_t n_tuples;         // 2^(L - 2K)
   uint32_t pos[2 * K];
   uint32_t mirror;           // 1: packed Hermitian mode
+  uint64_t tp_lo, tp_m;      // packed mode: transpose descriptor of the shard (TDesc below)
 };
 
 // K3 groups: a program of sub-ops (k = 1, 2 or 3) applied to 4^nq-member tuples (2 nq
@@ -43,6 +44,7 @@ struct GroupParams {
   uint64_t n_tuples;
   uint32_t pos[8];
   uint32_t mirror;           // 1: packed Hermitian mode
+  uint64_t tp_lo, tp_m;      // packed mode: transpose descriptor of the shard
   uint32_t dbg;              // profiling experiments only (env TANQ_DBG): 1 skip sub-ops,
                              // 2 skip HBM copies; 0 in production
   GroupSub sub[kMaxSub];
@@ -66,6 +68,7 @@ struct BlockParams {
   int32_t n_sub;
   int32_t pairs;             // warp pairs per CTA (smem-limited, <= kBlockMaxPairs)
   uint32_t mirror;           // packed Hermitian layout
+  uint64_t tp_lo, tp_m;      // packed mode: transpose descriptor of the shard
   uint32_t dbg;              // experiments only: 1 skip sub-ops, 2 skip HBM copies
   int32_t half_add;          // >= 0: one offset table for both warp halves, the second half
                              // adding half_add units; -1: a table per half
@@ -90,9 +93,22 @@ struct BlockParams {
   int32_t slot_off;          // uint16 offset of the 1024-entry slot table in the blob
 };
 
+// Transpose descriptor of a shard in the packed Hermitian layout.  The
+// transpose of a local element index e is  pair_swap(e & lo) | ((e & ~lo) ^ m):  the fully
+// local qubits occupy aligned (row, col) pairs below the boundary lo = 2^(2F) - 1, and above it
+// sit the row bits of the half-global qubits of the shard-local parity layout, whose global bit
+// holds r XOR c -- the transpose keeps the shard and flips the row bit where the shard's parity
+// bit is 1 (m).  One shard: lo = ~0, m = 0 (plain pair_swap).
+struct TDesc {
+  uint64_t lo = ~0ull;
+  uint64_t m = 0;
+};
+
 struct BitMap {               // physical bit of each logical bit (row q -> 2q, col q -> 2q+1)
   uint32_t phys[64];
   int nbits;                 // 2n
+  uint64_t par;              // qubits h whose col slot phys[2h+1] holds r_h XOR c_h (parity
+                             // layout: every global bit is such a parity bit)
 };
 
 // kernel launchers (all asynchronous on `st`)
@@ -102,7 +118,7 @@ cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st);
 cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStream_t st);
 size_t block_smem_bytes(int pairs, int blob_bytes);
 // packed Hermitian layout -> full layout (single shard, interleaved identity bit map)
-cudaError_t launch_unpack(double2* a, int L, cudaStream_t st);
+cudaError_t launch_unpack(double2* a, int L, TDesc td, cudaStream_t st);
 size_t group_frag_elems(int k);                               // double2 per sub-op matrix
 void group_make_frags(int k, const double2* S_member_order, double2* frag /*host*/);
 
@@ -123,6 +139,22 @@ cudaError_t launch_pack_quarter(const double2* a, double2* buf, int b0, int v0, 
                                 uint64_t first, uint64_t count, cudaStream_t st);
 cudaError_t launch_unpack_quarter(double2* a, const double2* buf, int b0, int v0, int b1, int v1,
                                   uint64_t first, uint64_t count, cudaStream_t st);
+
+// Parity-layout remap: half-global qubit h (local row bit x, global parity bit
+// a) trades places with fully local qubit v (row bit y, col bit z).  An element with local
+// bits (ex, ey, ez) on the shard whose bit a is s moves to the shard whose bit a is ey ^ ez, at
+// local bits (x, y, z) = (ey, ex, ex ^ s).  Octet = the 8 elements differing in x, y, z.
+// Single process: both shards of a pair (A: bit a = 0, B: 1) in one in-place kernel.
+cudaError_t launch_parity_swap(double2* A, double2* B, int L, int x, int y, int z,
+                               cudaStream_t st);
+// One process per shard: the staying elements (ey ^ ez == s) are permuted in place; the
+// leaving ones are packed as (octet, slot j = 2 ex + ey) and the partner's arrive in the
+// slots they vacate (elements [first, first + count) of that order; count, first % 4 == 0).
+cudaError_t launch_parity_stay(double2* a, int L, int x, int y, int z, int s, cudaStream_t st);
+cudaError_t launch_parity_pack(const double2* a, double2* buf, int L, int x, int y, int z, int s,
+                               uint64_t first, uint64_t count, cudaStream_t st);
+cudaError_t launch_parity_unpack(double2* a, const double2* buf, int L, int x, int y, int z,
+                                 int s, uint64_t first, uint64_t count, cudaStream_t st);
 
 // Paper vec index v = r + c 2^n  <->  physical index; gather / scatter the owned entries
 // of a range [first, first+count) of vec(rho) for shard `shard` (local bits L).
@@ -151,6 +183,7 @@ cudaError_t launch_sample(const double* cdf, int n, uint64_t seed, uint64_t shot
                           unsigned long long* out, cudaStream_t st);
 cudaError_t launch_add(double* dst, const double* src, uint64_t count, cudaStream_t st);
 // res[0] = max |a[P] - conj(a[pair_swap(P)])|, res[1] = max |a[P]| (bit patterns of doubles)
-cudaError_t launch_herm_check(const double2* a, int L, unsigned long long* res, cudaStream_t st);
+cudaError_t launch_herm_check(const double2* a, int L, TDesc td, unsigned long long* res,
+                              cudaStream_t st);
 
 }  // namespace tanq

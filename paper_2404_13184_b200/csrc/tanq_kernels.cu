@@ -17,6 +17,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "tanq_internal.h"
@@ -78,6 +79,13 @@ __device__ __forceinline__ uint64_t pair_swap(uint64_t x) {
   return ((x & 0x5555555555555555ull) << 1) | ((x >> 1) & 0x5555555555555555ull);
 }
 __device__ __forceinline__ double2 cj(double2 v) { return make_double2(v.x, -v.y); }
+// Transpose of an index from which r low bits (whole pairs below the pair boundary) have been
+// removed, under the shard's transpose descriptor (TDesc, tanq_internal.h): pairs below the
+// boundary swap, the half-global row bits above it flip by the shard mask.
+__device__ __forceinline__ uint64_t tpose(uint64_t x, uint64_t lo, uint64_t m, int r) {
+  const uint64_t l = lo >> r;
+  return pair_swap(x & l) | ((x & ~l) ^ (m >> r));
+}
 
 // Packed Hermitian layout: of each transpose pair {e, pair_swap(e)} only the
 // element with e <= pair_swap(e) is kept up to date (diagonal-type elements e = pair_swap(e)
@@ -93,11 +101,13 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 // orders all its elements against their transposes the same way: when that pair makes the
 // base the stored one, every element is read and written in place (the common case for the
 // canonical tiles the kernels visit) and the per-element test is skipped.
-__device__ __forceinline__ bool packed_tile_direct(uint64_t base, int hi) {
-  const uint64_t d = (base ^ (base >> 1)) & 0x5555555555555555ull;
+// (A differing pair counts at its lower position; a flipped half-global row bit at its own.)
+__device__ __forceinline__ bool packed_tile_direct(uint64_t base, int hi, uint64_t lo, uint64_t m) {
+  const uint64_t bt = tpose(base, lo, m, 0);
+  const uint64_t d = (base ^ bt) & (0x5555555555555555ull | ~lo);
   if (!d) return false;
   const int hb = 63 - __clzll(d);
-  return hb > hi && packed_stored(base, pair_swap(base));
+  return hb > hi && packed_stored(base, bt);
 }
 
 __device__ __forceinline__ void ld32(const double2* p, double2& a, double2& b) {
@@ -143,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, K == 2 ? 2 : 1)
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < p.n_tuples; t += stride) {
     uint64_t tm = t;
     if (p.mirror) {  // packed mode: only the canonical tuple of each transpose pair
-      tm = pair_swap(t);
+      tm = tpose(t, p.tp_lo, p.tp_m, 2 * K);
       if (tm < t) continue;
     }
     uint64_t base = t, basem = tm;
@@ -274,14 +284,14 @@ __global__ void __launch_bounds__(256, 2)
   // packed mode: the transpose of (tuple t, member m) is (pair_swap(t), pswap_c(m)); tiles
   // whose elements are all stored in place (packed_tile_direct) skip the per-element test
   auto tile_packed = [&](uint64_t tl) {
-    return p.mirror && !packed_tile_direct(base_of(tl * 8), hi_tile);
+    return p.mirror && !packed_tile_direct(base_of(tl * 8), hi_tile, p.tp_lo, p.tp_m);
   };
   auto load_tile = [&](uint64_t tl, double2* x, bool packed) {
     const uint64_t t = tl * 8 + r4;
     if (tl < n_tiles && t < p.n_tuples) {
       const uint64_t b = base_of(t);
       if (packed) {
-        const uint64_t bm = base_of(pair_swap(t));
+        const uint64_t bm = base_of(tpose(t, p.tp_lo, p.tp_m, 4));
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {  // one load per element: select the address first
           const uint64_t e = b + offB[ks], em = bm + member_off(pswap_c(4 * ks + c4));
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(256, 2)
   // the two tiles of a block belong to warps 2j, 2j+1 of one CTA
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
-      while (tl < n_tiles && (tl >> 1) > pair_swap(tl >> 1)) tl += nwarps;
+      while (tl < n_tiles && (tl >> 1) > tpose(tl >> 1, p.tp_lo, p.tp_m, 8)) tl += nwarps;
     return tl;
   };
 
@@ -330,13 +340,13 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
     const uint64_t t0 = tile * 8 + 2 * c4;
-    const bool self = p.mirror && (tile >> 1) == pair_swap(tile >> 1);
+    const bool self = p.mirror && (tile >> 1) == tpose(tile >> 1, p.tp_lo, p.tp_m, 8);
     if (self) named_bar(1 + ((threadIdx.x >> 5) >> 1), 64);  // both tiles' loads are done
     const uint64_t b0 = base_of(t0), b1 = base_of(t0 + 1);
     uint64_t bm0 = 0, bm1 = 0;
     if (pk_cur) {
-      bm0 = base_of(pair_swap(t0));
-      bm1 = base_of(pair_swap(t0 + 1));
+      bm0 = base_of(tpose(t0, p.tp_lo, p.tp_m, 4));
+      bm1 = base_of(tpose(t0 + 1, p.tp_lo, p.tp_m, 4));
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -673,7 +683,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   auto block_of = [&](uint64_t tl) { return (tl << TB) >> 4; };
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
-      while (tl < n_tiles && block_of(tl) > pair_swap(block_of(tl))) tl += tile_stride;
+      while (tl < n_tiles && block_of(tl) > tpose(block_of(tl), p.tp_lo, p.tp_m, MB + 4))
+        tl += tile_stride;
     return tl;
   };
   uint64_t tile = next_tile((uint64_t)blockIdx.x * WARPS + warp);
@@ -682,8 +693,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   // issue the tile's copies; returns the mask of elements copied from transpose positions
   auto issue_load = [&](uint64_t tl, double2* buf) {
     const uint64_t tb0 = insert_zeros(tl << TB, p.lo_mask, MB);
-    const uint64_t base = tb0 + lane_off, pbase = pair_swap(tb0) + lane_poff;
-    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+    const uint64_t base = tb0 + lane_off, pbase = tpose(tb0, p.tp_lo, p.tp_m, 0) + lane_poff;
+    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile, p.tp_lo, p.tp_m);
     unsigned mask = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -744,12 +755,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
       __syncwarp();
     }
-    const bool self = p.mirror && block_of(tile) == pair_swap(block_of(tile));
+    const bool self =
+        p.mirror && block_of(tile) == tpose(block_of(tile), p.tp_lo, p.tp_m, MB + 4);
     if (self) named_bar(1 + warp / WPB, 32 * WPB);  // the block's loads are all done
     if (!(p.dbg & 2)) {
       const uint64_t tb0 = insert_zeros(tile << TB, p.lo_mask, MB);
-      const uint64_t base = tb0 + lane_off, pbase = pair_swap(tb0) + lane_poff;
-      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+      const uint64_t base = tb0 + lane_off, pbase = tpose(tb0, p.tp_lo, p.tp_m, 0) + lane_poff;
+      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile, p.tp_lo, p.tp_m);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int tm = lane_tm | sIterTM[i];
@@ -885,7 +897,7 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
   const uint64_t n_tiles = (p.n_tuples + TT - 1) >> TTB;
   auto next_tile = [&](uint64_t tl) {
     if (p.mirror)
-      while (tl < n_tiles && tl > pair_swap(tl)) tl += gridDim.x;
+      while (tl < n_tiles && tl > tpose(tl, p.tp_lo, p.tp_m, MB + TTB)) tl += gridDim.x;
     return tl;
   };
   // shared index of tile element (tuple t, member m): warp sub-tile t / T, swizzled inside
@@ -895,8 +907,8 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
   };
   auto issue_load = [&](uint64_t tl, double2* buf) {
     const uint64_t tb0 = insert_zeros(tl << TTB, p.lo_mask, MB);
-    const uint64_t base = tb0 + thr_off, pbase = pair_swap(tb0) + thr_poff;
-    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+    const uint64_t base = tb0 + thr_off, pbase = tpose(tb0, p.tp_lo, p.tp_m, 0) + thr_poff;
+    const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile, p.tp_lo, p.tp_m);
     unsigned mask = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -951,9 +963,9 @@ __global__ void __launch_bounds__(WARPS * 32, (NBUF == 2 ? 12 : 16) / WARPS)
     __syncthreads();
     if (!(p.dbg & 2)) {
       const uint64_t tb0 = insert_zeros(tile << TTB, p.lo_mask, MB);
-      const uint64_t base = tb0 + thr_off, pbase = pair_swap(tb0) + thr_poff;
-      const bool self = pair_swap(tile) == tile;
-      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile);
+      const uint64_t base = tb0 + thr_off, pbase = tpose(tb0, p.tp_lo, p.tp_m, 0) + thr_poff;
+      const bool self = tpose(tile, p.tp_lo, p.tp_m, MB + TTB) == tile;
+      const bool packed = p.mirror && !packed_tile_direct(tb0, hi_tile, p.tp_lo, p.tp_m);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int tm = thr_tm | sIterTM[i];
@@ -1051,17 +1063,17 @@ cudaError_t launch_group3(double2* a, const GroupParams& p, cudaStream_t st) {
 }
 
 // Packed -> full layout: every element the packed layout does not keep gets conj(transpose).
-__global__ void unpack_kernel(double2* __restrict__ a, uint64_t n) {
+__global__ void unpack_kernel(double2* __restrict__ a, uint64_t n, uint64_t lo, uint64_t m) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += stride) {
-    const uint64_t em = pair_swap(e);
+    const uint64_t em = tpose(e, lo, m, 0);
     if (!packed_stored(e, em)) a[e] = cj(a[em]);
   }
 }
 
-cudaError_t launch_unpack(double2* a, int L, cudaStream_t st) {
+cudaError_t launch_unpack(double2* a, int L, TDesc td, cudaStream_t st) {
   const uint64_t n = (uint64_t)1 << L;
-  unpack_kernel<<<grid_for(n, kThreads, 148ull * 16), kThreads, 0, st>>>(a, n);
+  unpack_kernel<<<grid_for(n, kThreads, 148ull * 16), kThreads, 0, st>>>(a, n, td.lo, td.m);
   return cudaGetLastError();
 }
 
@@ -1096,6 +1108,129 @@ cudaError_t launch_swap_halves(double2* A, double2* B, int L, int b, int va, int
   uint64_t half = (uint64_t)1 << (L - 1);
   swap_halves_kernel<<<grid_for(half, kThreads, 148ull * 32), kThreads, 0, st>>>(A, B, half, b, va,
                                                                                vb);
+  return cudaGetLastError();
+}
+
+// ---- parity-layout remap (tanq_internal.h) ----
+struct Oct {
+  uint64_t lo0, lo1, lo2;  // (1 << p) - 1 of the sorted positions of x, y, z
+  uint64_t bx, by, bz;
+  __device__ uint64_t base(uint64_t o) const {
+    o = ((o & ~lo0) << 1) | (o & lo0);
+    o = ((o & ~lo1) << 1) | (o & lo1);
+    return ((o & ~lo2) << 1) | (o & lo2);
+  }
+  __device__ uint64_t off(int i) const {  // i: bit 0 = x, bit 1 = y, bit 2 = z
+    return ((i & 1) ? bx : 0) | ((i & 2) ? by : 0) | ((i & 4) ? bz : 0);
+  }
+};
+static Oct make_oct(int x, int y, int z) {
+  int p[3] = {x, y, z};
+  std::sort(p, p + 3);
+  Oct o;
+  o.lo0 = ((uint64_t)1 << p[0]) - 1;
+  o.lo1 = ((uint64_t)1 << p[1]) - 1;
+  o.lo2 = ((uint64_t)1 << p[2]) - 1;
+  o.bx = (uint64_t)1 << x;
+  o.by = (uint64_t)1 << y;
+  o.bz = (uint64_t)1 << z;
+  return o;
+}
+// destination octet slot of slot i (ex, ey, ez) from a shard with parity bit s
+__device__ __forceinline__ int par_dst(int i, int s) {
+  const int ex = i & 1, ey = (i >> 1) & 1;
+  return ey | (ex << 1) | ((ex ^ s) << 2);
+}
+__device__ __forceinline__ int par_leaves(int i, int s) { return (((i >> 1) ^ (i >> 2)) & 1) != s; }
+
+__global__ void parity_swap_kernel(double2* __restrict__ A, double2* __restrict__ B, uint64_t noct,
+                                   Oct oc) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < noct; o += stride) {
+    const uint64_t b = oc.base(o);
+    double2 va[8], vb[8], oa[8], ob[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      va[i] = A[b + oc.off(i)];
+      vb[i] = B[b + oc.off(i)];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // A has parity bit 0, B 1; an element lands on shard ey ^ ez
+      if (par_leaves(i, 0)) ob[par_dst(i, 0)] = va[i]; else oa[par_dst(i, 0)] = va[i];
+      if (par_leaves(i, 1)) oa[par_dst(i, 1)] = vb[i]; else ob[par_dst(i, 1)] = vb[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i != 0 && i != 7) A[b + oc.off(i)] = oa[i];  // slots 000 / 111 of A keep their element
+      if (i != 4 && i != 3) B[b + oc.off(i)] = ob[i];  // (ex, ey, ez) = 001 / 110 of B too
+    }
+  }
+}
+
+cudaError_t launch_parity_swap(double2* A, double2* B, int L, int x, int y, int z,
+                               cudaStream_t st) {
+  const uint64_t noct = (uint64_t)1 << (L - 3);
+  parity_swap_kernel<<<grid_for(noct, kThreads, 148ull * 16), kThreads, 0, st>>>(A, B, noct,
+                                                                                make_oct(x, y, z));
+  return cudaGetLastError();
+}
+
+__global__ void parity_stay_kernel(double2* __restrict__ a, uint64_t noct, Oct oc, int s) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < noct; o += stride) {
+    const uint64_t b = oc.base(o);
+    double2 v[8], w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (!par_leaves(i, s) && par_dst(i, s) != i) v[i] = a[b + oc.off(i)];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (!par_leaves(i, s) && par_dst(i, s) != i) w[par_dst(i, s)] = v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (!par_leaves(i, s) && par_dst(i, s) != i) a[b + oc.off(par_dst(i, s))] = w[par_dst(i, s)];
+  }
+}
+
+// leaving slot j (0..3) of a shard with parity bit s: ex = j >> 1, ey = j & 1, ez = ey ^ 1 ^ s
+__device__ __forceinline__ int par_slot(int j, int s) {
+  const int ex = j >> 1, ey = j & 1;
+  return ex | (ey << 1) | ((ey ^ 1 ^ s) << 2);
+}
+
+__global__ void parity_pack_kernel(const double2* __restrict__ a, double2* __restrict__ buf,
+                                   Oct oc, int s, uint64_t first, uint64_t count, int dir) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t e = first + i;
+    const uint64_t b = oc.base(e >> 2);
+    const int j = (int)(e & 3);
+    if (dir == 0) {
+      buf[i] = a[b + oc.off(par_slot(j, s))];
+    } else {  // received slot j of the partner (parity bit s ^ 1)
+      const_cast<double2*>(a)[b + oc.off(par_dst(par_slot(j, s ^ 1), s ^ 1))] = buf[i];
+    }
+  }
+}
+
+cudaError_t launch_parity_stay(double2* a, int L, int x, int y, int z, int s, cudaStream_t st) {
+  const uint64_t noct = (uint64_t)1 << (L - 3);
+  parity_stay_kernel<<<grid_for(noct, kThreads, 148ull * 16), kThreads, 0, st>>>(
+      a, noct, make_oct(x, y, z), s);
+  return cudaGetLastError();
+}
+cudaError_t launch_parity_pack(const double2* a, double2* buf, int L, int x, int y, int z, int s,
+                               uint64_t first, uint64_t count, cudaStream_t st) {
+  (void)L;
+  parity_pack_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, buf, make_oct(x, y, z), s, first, count, 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_parity_unpack(double2* a, const double2* buf, int L, int x, int y, int z,
+                                 int s, uint64_t first, uint64_t count, cudaStream_t st) {
+  (void)L;
+  parity_pack_kernel<<<grid_for(count, kThreads, 148ull * 32), kThreads, 0, st>>>(
+      a, const_cast<double2*>(buf), make_oct(x, y, z), s, first, count, 1);
   return cudaGetLastError();
 }
 
@@ -1167,6 +1302,10 @@ __device__ __forceinline__ uint64_t vec_to_phys(uint64_t v, const BitMap& bm, in
     P |= ((v >> q) & 1ull) << bm.phys[2 * q];
     P |= ((v >> (n + q)) & 1ull) << bm.phys[2 * q + 1];
   }
+  for (uint64_t h = bm.par; h; h &= h - 1) {  // parity layout: the col slot holds r XOR c
+    const int q = __ffsll((long long)h) - 1;
+    P ^= ((v >> q) & 1ull) << bm.phys[2 * q + 1];
+  }
   return P;
 }
 
@@ -1216,7 +1355,8 @@ __device__ __forceinline__ uint64_t diag_phys(uint64_t x, const BitMap& bm, int 
   uint64_t P = 0;
   for (int q = 0; q < n; ++q) {
     uint64_t b = (x >> q) & 1ull;
-    P |= (b << bm.phys[2 * q]) | (b << bm.phys[2 * q + 1]);
+    P |= b << bm.phys[2 * q];
+    if (!((bm.par >> q) & 1ull)) P |= b << bm.phys[2 * q + 1];  // parity r XOR c = 0
   }
   return P;
 }
@@ -1309,6 +1449,10 @@ __global__ void expect_kernel(const double2* __restrict__ a, double2* partial,
       P |= ((row >> q) & 1ull) << bm.phys[2 * q];
       P |= ((col >> q) & 1ull) << bm.phys[2 * q + 1];
     }
+    for (uint64_t h = bm.par; h; h &= h - 1) {
+      const int q = __ffsll((long long)h) - 1;
+      P ^= ((row >> q) & 1ull) << bm.phys[2 * q + 1];
+    }
     if ((P >> L) != shard) continue;
     double2 v = a[P & lmask];
     double sgn = (__popcll(col & zm) & 1) ? -1.0 : 1.0;
@@ -1347,12 +1491,12 @@ __global__ void add_kernel(double* dst, const double* src, uint64_t count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride)
     dst[i] += src[i];
 }
-__global__ void herm_check_kernel(const double2* __restrict__ a, uint64_t N,
-                                  unsigned long long* res) {
+__global__ void herm_check_kernel(const double2* __restrict__ a, uint64_t N, uint64_t tlo,
+                                  uint64_t tm, unsigned long long* res) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   double d = 0.0, m = 0.0;
   for (uint64_t P = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; P < N; P += stride) {
-    const double2 x = a[P], y = a[pair_swap(P)];
+    const double2 x = a[P], y = a[tpose(P, tlo, tm, 0)];
     d = fmax(d, fmax(fabs(x.x - y.x), fabs(x.y + y.y)));
     m = fmax(m, fmax(fabs(x.x), fabs(x.y)));
   }
@@ -1366,9 +1510,11 @@ __global__ void herm_check_kernel(const double2* __restrict__ a, uint64_t N,
   }
 }
 
-cudaError_t launch_herm_check(const double2* a, int L, unsigned long long* res, cudaStream_t st) {
+cudaError_t launch_herm_check(const double2* a, int L, TDesc td, unsigned long long* res,
+                              cudaStream_t st) {
   const uint64_t N = (uint64_t)1 << L;
-  herm_check_kernel<<<grid_for(N, kThreads, 148ull * 8), kThreads, 0, st>>>(a, N, res);
+  herm_check_kernel<<<grid_for(N, kThreads, 148ull * 8), kThreads, 0, st>>>(a, N, td.lo, td.m,
+                                                                           res);
   return cudaGetLastError();
 }
 

@@ -86,6 +86,7 @@ class tanq_block_params(ctypes.Structure):
     """Mirror of tanq::BlockParams (csrc/tanq_internal.h) for tanq_plan_block_program."""
     _fields_ = [("blob", ctypes.c_void_p), ("blob_bytes", ctypes.c_int32),
                 ("n_sub", ctypes.c_int32), ("pairs", ctypes.c_int32), ("mirror", ctypes.c_uint32),
+                ("tp_lo", ctypes.c_uint64), ("tp_m", ctypes.c_uint64),
                 ("dbg", ctypes.c_uint32), ("half_add", ctypes.c_int32),
                 ("n_blocks", ctypes.c_uint64), ("lo_mask", ctypes.c_uint64 * 10),
                 ("piece_goff", ctypes.c_uint64 * 64), ("piece_start", ctypes.c_uint16 * 64),
@@ -99,7 +100,8 @@ class tanq_info(ctypes.Structure):
     _fields_ = [("n_qubits", ctypes.c_int32), ("n_shards", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("local_bits", ctypes.c_int32), ("rowpos", ctypes.c_int32 * 32),
-                ("colpos", ctypes.c_int32 * 32), ("shard_bytes", ctypes.c_uint64)]
+                ("colpos", ctypes.c_int32 * 32), ("shard_bytes", ctypes.c_uint64),
+                ("parity_qubits", ctypes.c_uint64)]
 
 
 class tanq_kernel_prof(ctypes.Structure):
@@ -500,7 +502,7 @@ class Simulator:
         return {"n_qubits": i.n_qubits, "n_shards": i.n_shards, "world_size": i.world_size,
                 "rank": i.rank, "local_bits": i.local_bits,
                 "rowpos": list(i.rowpos[:i.n_qubits]), "colpos": list(i.colpos[:i.n_qubits]),
-                "shard_bytes": i.shard_bytes}
+                "shard_bytes": i.shard_bytes, "parity_qubits": i.parity_qubits}
 
     def set_stream(self, stream_ptr: int, shard: int = 0):
         _check(lib().tanq_set_stream(self.h, shard, ctypes.c_void_p(stream_ptr)), "tanq_set_stream")

@@ -55,11 +55,54 @@ def _half_offsets(L, b, v):
     return ((e >> b) << (b + 1)) | (v << b) | (e & ((1 << b) - 1))
 
 
-def _worker(rank, world, port, n, seed, out_path):
+def _init_layout(n, g, parity):
+    """The engine's initial layout (tanq_host.cpp init_layout): identity bit map; in the parity
+    layout the top g qubits are half-global (row bit local above the pairs, global bit = r^c)."""
+    phys = list(range(2 * n))
+    par = 0
+    if parity and n - g >= 5:  # smaller registers keep the bit layout
+        F, L = n - g, 2 * n - g
+        for i in range(g):
+            h = F + i
+            phys[2 * h], phys[2 * h + 1] = 2 * F + i, L + i
+            par |= 1 << h
+    return phys, par
+
+
+def _parity_slot(j, s):
+    """Leaving slot j of a shard with parity bit s: (ex, ey, ez) = (j >> 1, j & 1, ey ^ 1 ^ s)."""
+    ex, ey = j >> 1, j & 1
+    return ex, ey, ey ^ 1 ^ s
+
+
+def _parity_remap(shard, L, x, y, z, s, exchange):
+    """DESIGN.md §7 parity remap on one shard (parity bit s of the swapped global bit): the
+    leaving half (ey ^ ez != s) goes to the partner in (octet, slot) order, the staying elements
+    and the arriving ones land at bits (x, y, z) = (ey, ex, ex ^ s_sender)."""
+    o = _insert_zeros(np.arange(1 << (L - 3), dtype=np.int64), [x, y, z])
+
+    def at(bx, by, bz):
+        return o | (bx << x) | (by << y) | (bz << z)
+    send = np.stack([shard[at(*_parity_slot(j, s))] for j in range(4)], axis=1).reshape(-1)
+    recv = exchange(send).reshape(-1, 4)
+    new = shard.copy()
+    for ex in (0, 1):
+        for ey in (0, 1):
+            ez = ey ^ s  # staying
+            new[at(ey, ex, ex ^ s)] = shard[at(ex, ey, ez)]
+    sp = s ^ 1
+    for j in range(4):
+        ex, ey, _ = _parity_slot(j, sp)
+        new[at(ey, ex, ex ^ sp)] = recv[:, j]
+    shard[:] = new
+
+
+def _worker(rank, world, port, n, seed, out_path, layout):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["TANQ_LAYOUT"] = layout
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2404_13184_b200.tanq import Plan
     c = W.random_circuit(n, 40, seed=seed, kmax=3, allow_matrix=True)
@@ -67,16 +110,36 @@ def _worker(rank, world, port, n, seed, out_path):
     plan = Plan(None, c, nm, fuse=2, k_max=3, world_size=world)
     ops = plan.ops()
     sched = plan.schedule(world)
-    L = 2 * n - (world.bit_length() - 1)
-    phys = list(range(2 * n))
+    g = world.bit_length() - 1
+    L = 2 * n - g
+    phys, par = _init_layout(n, g, layout == "parity")
     shard = np.zeros(1 << L, dtype=np.complex128)
     if rank == 0:
         shard[0] = 1.0
     n_swaps = 0
+
+    def exchange(partner, arr):
+        send = torch.from_numpy(np.ascontiguousarray(arr).view(np.float64))
+        recv = torch.empty_like(send)
+        reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
+        for r in reqs:
+            r.wait()
+        return recv.numpy().view(np.complex128)
+
     for kind, x, y in sched:
         if kind == 0:
             qs, S = ops[x]
             _apply_op(shard, L, qs, S, phys)
+        elif kind == 2:  # parity remap: half-global qubit x <-> fully local qubit y
+            h, v = x, y
+            bx, ba, by, bz = phys[2 * h], phys[2 * h + 1], phys[2 * v], phys[2 * v + 1]
+            assert (par >> h) & 1 and not (par >> v) & 1 and ba >= L > max(bx, by, bz)
+            gb = ba - L
+            _parity_remap(shard, L, bx, by, bz, (rank >> gb) & 1,
+                          lambda arr: exchange(rank ^ (1 << gb), arr))
+            phys[2 * h], phys[2 * h + 1], phys[2 * v], phys[2 * v + 1] = by, bz, bx, ba
+            par ^= (1 << h) | (1 << v)
+            n_swaps += 1
         else:
             a, b = x, y
             gb = a - L
@@ -102,6 +165,8 @@ def _worker(rank, world, port, n, seed, out_path):
         for q in range(n):
             P |= ((v >> q) & 1) << phys[2 * q]
             P |= ((v >> (n + q)) & 1) << phys[2 * q + 1]
+            if (par >> q) & 1:  # parity layout: the global bit holds r ^ c
+                P ^= ((v >> q) & 1) << phys[2 * q + 1]
         np.save(out_path, full[P])
         with open(out_path + ".swaps", "w") as f:
             f.write(str(n_swaps))
@@ -109,12 +174,14 @@ def _worker(rank, world, port, n, seed, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,seed", [(2, 4, 1), (2, 5, 2), (4, 5, 3), (4, 4, 4)])
-def test_distributed_schedule_matches_oracle(tmp_path, world, n, seed):
+@pytest.mark.parametrize("world,n,seed,layout", [
+    (2, 4, 1, "bits"), (2, 5, 2, "bits"), (4, 5, 3, "bits"), (4, 4, 4, "bits"),
+    (2, 6, 5, "parity"), (2, 7, 6, "parity"), (4, 7, 7, "parity"), (4, 8, 8, "parity")])
+def test_distributed_schedule_matches_oracle(tmp_path, world, n, seed, layout):
     import torch.multiprocessing as mp
     from oracle import dense
     out = str(tmp_path / "vec.npy")
-    mp.start_processes(_worker, args=(world, _free_port(), n, seed, out), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), n, seed, out, layout), nprocs=world,
                        join=True, start_method="spawn")
     vec = np.load(out)
     c = W.random_circuit(n, 40, seed=seed, kmax=3, allow_matrix=True)
@@ -125,6 +192,54 @@ def test_distributed_schedule_matches_oracle(tmp_path, world, n, seed):
 
 
 def test_schedule_makes_every_op_local():
+    """Parity layout (the default): every remap trades a half-global qubit the next op targets
+    for a fully local one it does not; every op then sees all its bits local."""
+    from paper_2404_13184_b200.tanq import Plan
+    for cfg, n, world in ((4, 16, 2), (4, 16, 8), (5, 18, 8), (3, 14, 4)):
+        c, nm = W.config_workload(cfg, n=n)
+        plan = Plan(None, c, nm, world_size=world)
+        g = world.bit_length() - 1
+        L = 2 * n - g
+        phys, par = _init_layout(n, g, True)
+        ops = plan.ops()
+        seen = 0
+        for kind, x, y in plan.schedule(world):
+            if kind == 2:
+                assert (par >> x) & 1 and not (par >> y) & 1
+                assert x in ops[seen][0] and y not in ops[seen][0]
+                bx, ba, by, bz = phys[2 * x], phys[2 * x + 1], phys[2 * y], phys[2 * y + 1]
+                phys[2 * x], phys[2 * x + 1], phys[2 * y], phys[2 * y + 1] = by, bz, bx, ba
+                par ^= (1 << x) | (1 << y)
+            else:
+                assert kind == 0 and x == seen
+                seen += 1
+                for q in ops[x][0]:
+                    assert phys[2 * q] < L and phys[2 * q + 1] < L and not (par >> q) & 1
+            # invariant: fully local qubits on aligned pairs below 2(n-g), row bits above
+            for q in range(n):
+                if (par >> q) & 1:
+                    assert 2 * (n - g) <= phys[2 * q] < L <= phys[2 * q + 1]
+                else:
+                    assert phys[2 * q] // 2 == phys[2 * q + 1] // 2 < n - g
+        assert seen == len(ops)
+
+
+def test_schedule_makes_every_op_local_bits_layout():
+    """The plain bit layout (TANQ_LAYOUT=bits, read once per process: a subprocess)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = [%r, %r]; "
+            "from test_dist_gloo import _bits_schedule_check as f; f()"
+            % (ROOT, os.path.join(ROOT, "tests")))
+    env = dict(os.environ, TANQ_LAYOUT="bits")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bits_schedule_check():
     from paper_2404_13184_b200.tanq import Plan
     for cfg, n, world in ((4, 16, 2), (4, 16, 8), (5, 18, 8), (3, 14, 4)):
         c, nm = W.config_workload(cfg, n=n)

@@ -38,7 +38,9 @@ def shim(tmp_path_factory):
 @pytest.mark.parametrize("world,n,seed,batch,xlog", [
     (2, 6, 5, "1", "23"), (2, 7, 6, "1", "23"), (4, 6, 7, "1", "23"), (8, 6, 8, "1", "23"),
     (4, 7, 9, "1", "23"), (4, 6, 7, "0", "23"), (8, 6, 8, "0", "23"),
-    (2, 7, 6, "1", "5"), (4, 7, 9, "1", "6"), (8, 6, 8, "0", "4")])
+    (2, 7, 6, "1", "5"), (4, 7, 9, "1", "6"), (8, 6, 8, "0", "4"),
+    # shard-local parity layout with the packed kernels (>= 6 fully local qubits)
+    (2, 8, 10, "1", "23"), (4, 8, 11, "1", "6"), (8, 9, 12, "1", "23"), (2, 9, 13, "1", "5")])
 def test_dist_remap_parity(shim, world, n, seed, batch, xlog):
     """batch = 1: two swaps of one op run as one 4-way exchange (remap_swap2); 0: pairwise.
     xlog: staging slot of 2^xlog amplitudes -- small slots run the pipelined exchange over
@@ -58,7 +60,7 @@ def test_dist_remap_parity(shim, world, n, seed, batch, xlog):
     print(line[-1])
 
 
-@pytest.mark.parametrize("world,config,n", [(8, 5, 8), (4, 4, 7)])
+@pytest.mark.parametrize("world,config,n", [(8, 5, 8), (4, 4, 7), (2, 4, 9), (8, 5, 9)])
 def test_dist_config_workloads(shim, world, config, n):
     """BASELINE configs 5 (VQE ansatz + its Pauli-string Hamiltonian, the 8-GPU config) and 4
     (QPE with calibrated noise + readout) scaled down, on `world` ranks: state, readout-noisy

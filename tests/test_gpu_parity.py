@@ -161,6 +161,53 @@ def test_virtual_shards_remap(Sim, shards, seed):
     assert abs(e - dense.expect_pauli(ref, n, 0b101, 0b110)) < ABS
 
 
+@pytest.mark.parametrize("n,shards,kmax,seed", [
+    (8, 2, 3, 0), (8, 4, 3, 1), (9, 8, 3, 2), (9, 2, 4, 3), (10, 4, 3, 4), (10, 2, 2, 5)])
+def test_virtual_shards_parity_packed(Sim, n, shards, kmax, seed):
+    """Shard-local parity layout: with >= 6 fully local qubits every shard runs
+    the packed Hermitian kernels (per-shard transpose descriptor), remaps trade a half-global
+    qubit for a local one (parity_swap_kernel), and the result matches the oracle."""
+    c = W.random_circuit(n, 70, seed=900 + seed, kmax=3)
+    nm = W.synthetic_calibration(c, seed, depol=True, thermal=True, overrot=True)
+    nm.order = seed % 2
+    ref = dense.run(c, nm)
+    with Sim(n, shards) as sim:
+        g = shards.bit_length() - 1
+        assert bin(sim.info()["parity_qubits"]).count("1") == g
+        st = sim.run_circuit(c, nm, fuse=2, k_max=kmax)
+        assert st["n_remaps"] > 0
+        p = sim.probs(dense.readout_of(nm))                   # packed: diagonal only
+        z = sim.expect_pauli(0, (1 << n) - 1)                # Z string on every qubit
+        e = sim.expect_pauli(0b11 << (n - 2), 0b101 << (n - 3))  # X/Y on the half-global qubits
+        got = rho_of(sim, n)
+        info = sim.info()
+    assert_parity(got, ref)
+    np.testing.assert_allclose(p, dense.probs(ref, n, dense.readout_of(nm)), atol=ABS)
+    assert abs(z - dense.expect_pauli(ref, n, 0, (1 << n) - 1)) < ABS
+    assert abs(e - dense.expect_pauli(ref, n, 0b11 << (n - 2), 0b101 << (n - 3))) < ABS
+    # layout invariant after the remaps: fully local qubits on aligned pairs, row bits above
+    F = n - g
+    for q in range(n):
+        if (info["parity_qubits"] >> q) & 1:
+            assert 2 * F <= info["rowpos"][q] < info["local_bits"] <= info["colpos"][q]
+        else:
+            assert info["rowpos"][q] // 2 == info["colpos"][q] // 2 < F
+
+
+def test_virtual_shards_parity_config4(Sim):
+    """QPE with calibrated noise (config 4 scaled to n = 9) on 2 and 4 shards in the parity
+    layout, with the packed kernels, against the oracle: state, readout-noisy probabilities."""
+    c, nm = W.config_workload(4, n=9)
+    ref = dense.run(c, nm)
+    for shards in (2, 4):
+        with Sim(9, shards) as sim:
+            st = sim.run_circuit(c, nm)
+            assert st["n_remaps"] > 0
+            np.testing.assert_allclose(sim.probs(dense.readout_of(nm)),
+                                       dense.probs(ref, 9, dense.readout_of(nm)), atol=ABS)
+            assert_parity(rho_of(sim, 9), ref)
+
+
 def test_config2_qft10_thermal_overrotation(Sim):
     c, nm = W.config_workload(2)
     ref = dense.run(c, nm)

@@ -314,6 +314,37 @@ __device__ __forceinline__ void blk_sub_k2(double2* X, const double* F, const ui
   }
 }
 
+// Sparse k = 2 sub-op (DFMA, one 16-member tuple per lane): the noisy superoperators of
+// Pauli-frame gates (CX, CP, RZ, X with depolarizing / thermal noise) keep 36-40 of their 256
+// entries, where the dense DMMA form spends 768 multiply-adds per tuple.  F: the nonzeros
+// (double2, row by row) then the uint16 row starts [17]; T[e * rows + trow]: this lane's
+// shared-memory slot of entry e's input member, T[(nnz + i) * rows + trow]: of output member i.
+// Each lane reads and writes only its own tuple, so no lane waits for another.
+__device__ __forceinline__ void blk_sub_k2s(double2* X, const double* F, const uint16_t* T,
+                                            int trow, int rows, int nnz) {
+  const double2* sv = reinterpret_cast<const double2*>(F);
+  const uint16_t* rs = reinterpret_cast<const uint16_t*>(sv + nnz);
+  double2 y[16];
+  int e = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    double yr = 0.0, yi = 0.0;
+    const int end = rs[i + 1];
+    for (; e < end; ++e) {
+      const double2 sc = sv[e];
+      const double2 x = X[T[e * rows + trow]];
+      yr = fma(sc.x, x.x, yr);
+      yr = fma(-sc.y, x.y, yr);
+      yi = fma(sc.x, x.y, yi);
+      yi = fma(sc.y, x.x, yi);
+    }
+    y[i] = make_double2(yr, yi);
+  }
+  const uint16_t* To = T + nnz * rows + trow;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) X[To[i * rows]] = y[i];
+}
+
 // k = 1 sub-op (4x4 complex, DFMA): T = this lane's 16 offsets [j column][i member].
 __device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const uint16_t* T,
                                            int trow, int rows) {
@@ -488,7 +519,9 @@ __global__ void __launch_bounds__(384, 1)
         const BlockSub& g = p.sub[q];
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
-        if (g.k == 2)
+        if (g.k == 2 && g.nnz)
+          blk_sub_k2s(Xh, F, T, trow, trows, g.nnz);
+        else if (g.k == 2)
           blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
@@ -653,7 +686,9 @@ __global__ void __launch_bounds__(384, 1)
         const BlockSub& g = p.sub[q];
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
-        if (g.k == 2)
+        if (g.k == 2 && g.nnz)
+          blk_sub_k2s(Xh, F, T, trow, 64, g.nnz);
+        else if (g.k == 2)
           blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, 64);
         else
           blk_sub_k1(Xh, F, T, trow, 64);

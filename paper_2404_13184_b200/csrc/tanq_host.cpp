@@ -1345,7 +1345,21 @@ bool block_enabled() {
   return on == 1;
 }
 
-size_t block_sub_bytes(int k) { return k == 2 ? 768 * 8 + 2 * 32 * 32 * 2 : 32 * 8 + 2 * 32 * 16 * 2; }
+// sparse k = 2 sub-ops (DFMA, tanq_block.cu blk_sub_k2s) take superoperators with at most
+// this many nonzeros (env TANQ_SPARSE_MAX; 0 = always DMMA)
+int sparse_max() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TANQ_SPARSE_MAX");
+    v = e ? std::max(0, std::min(64, std::atoi(e))) : 64;
+  }
+  return v;
+}
+size_t sparse_sub_bytes(int nnz) { return (size_t)16 * nnz + 48 + (((size_t)(nnz + 16) * 64 * 2 + 15) & ~(size_t)15); }
+size_t block_sub_bytes(int k) {
+  return k == 2 ? std::max<size_t>(768 * 8 + 2 * 32 * 32 * 2, sparse_sub_bytes(64))
+                : 32 * 8 + 2 * 32 * 16 * 2;
+}
 
 size_t block_blob_bytes(const FusedOp& op) {  // upper bound (incl. the TMA slot table)
   size_t b = 2048;
@@ -1767,8 +1781,75 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     for (int c : scol_bits[i])
       if (std::find(cols.begin(), cols.end(), c) == cols.end()) cols.push_back(c);
     g.a_off = (int)(off / 8);
+    g.nnz = 0;
     uint16_t* T;
-    if (sb.k == 2) {
+    int nnz = 0;
+    if (sb.k == 2)
+      for (const double2& v : Sm) nnz += (v.x != 0.0 || v.y != 0.0) ? 1 : 0;
+    if (sb.k == 2 && nnz > 0 && nnz <= sparse_max()) {
+      // sparse DFMA sub-op: lane = tuple (the 5 block bits outside the sub-op and the half
+      // bit); the 3 lane bits of a quarter warp are chosen for distinct banks
+      g.nnz = nnz;
+      double2* sv = reinterpret_cast<double2*>(blob + off);
+      uint16_t rs[17];
+      std::vector<int> ein;  // input member of entry e
+      for (int r = 0, e = 0; r < 16; ++r) {
+        rs[r] = (uint16_t)e;
+        for (int c = 0; c < 16; ++c) {
+          const double2 v = Sm[(size_t)r * 16 + c];
+          if (v.x != 0.0 || v.y != 0.0) {
+            sv[e++] = v;
+            ein.push_back(c);
+          }
+        }
+        rs[16] = (uint16_t)e;
+      }
+      off += (size_t)16 * nnz;
+      std::memcpy(blob + off, rs, sizeof(rs));
+      off += 48;
+      g.t_off = (int)(off / 2);
+      T = reinterpret_cast<uint16_t*>(blob + off);
+      std::vector<int> tb(scol_bits[i]);  // 5 tuple bits
+      {  // order: the 3 bits that spread a quarter warp over the most banks first
+        int best = 1 << 30;
+        std::vector<int> best_tb = tb;
+        for (int x = 0; x < 5; ++x)
+          for (int y = x + 1; y < 5; ++y)
+            for (int z = y + 1; z < 5; ++z) {
+              std::vector<int> cand{tb[x], tb[y], tb[z]};
+              for (int u = 0; u < 5; ++u)
+                if (u != x && u != y && u != z) cand.push_back(tb[u]);
+              int cost = 0;
+              for (int m = 0; m < 16; ++m)
+                for (int ph = 0; ph < 4; ++ph) {
+                  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+                  for (int l = 0; l < 8; ++l) {
+                    const int idx = deposit(smem_bits[i].data(), 4, m) |
+                                    deposit(cand.data(), 5, l | (ph << 3));
+                    mx = std::max(mx, ++cnt[slot(idx) & 7]);
+                  }
+                  cost += mx;
+                }
+              if (cost < best) {
+                best = cost;
+                best_tb = cand;
+              }
+            }
+        tb = best_tb;
+      }
+      const int rows = halves * 32;
+      for (int h = 0; h < halves; ++h)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int tup = deposit(tb.data(), 5, lane) | (h << half);
+          for (int e = 0; e < nnz; ++e)
+            T[(size_t)e * rows + h * 32 + lane] =
+                (uint16_t)slot(deposit(smem_bits[i].data(), 4, ein[e]) | tup);
+          for (int m = 0; m < 16; ++m)
+            T[(size_t)(nnz + m) * rows + h * 32 + lane] =
+                (uint16_t)slot(deposit(smem_bits[i].data(), 4, m) | tup);
+        }
+      off += ((size_t)(nnz + 16) * rows * 2 + 15) & ~(size_t)15;
+    } else if (sb.k == 2) {
       int in_bits[4] = {ch.k0, ch.k1, 0, 0}, out_bits[4] = {ch.o0, 0, 0, ch.o3};
       for (int t = 0, a = 2, b = 1; t < 4; ++t) {
         const int bb = smem_bits[i][t];

@@ -58,9 +58,12 @@ static constexpr int kBlockMaxSub = 12;
 struct BlockSub {
   int32_t k;       // 1 or 2
   int32_t a_off;   // doubles: k=2 fragments [3][4 ks][32 lanes][2 mt] (a, -(a+b), b-a);
-                   // k=1: 16 double2
-  int32_t t_off;   // uint16: per-lane shared-memory offset tables [1|2 halves][32][32|16]
+                   // k=1: 16 double2; sparse k=2: nnz double2 values (row-major) + uint16
+                   // row starts [17]
+  int32_t t_off;   // uint16: per-lane shared-memory offset tables [1|2 halves][32][32|16];
+                   // sparse k=2: [nnz + 16][rows] (entry inputs, then the 16 outputs)
   int32_t tmask;   // k=2: nonzero 8x4 A tiles, bit mt * 4 + ks (zero tiles are skipped)
+  int32_t nnz;     // k=2: > 0 -> sparse DFMA sub-op (one tuple per lane), 0 -> DMMA
 };
 struct BlockParams {
   const void* blob;          // sub-op fragments + offset tables (device), copied to shared

@@ -79,7 +79,7 @@ class tanq_run_stats(ctypes.Structure):
 
 class tanq_block_sub(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("a_off", ctypes.c_int32), ("t_off", ctypes.c_int32),
-                ("tmask", ctypes.c_int32)]
+                ("tmask", ctypes.c_int32), ("nnz", ctypes.c_int32)]
 
 
 class tanq_block_params(ctypes.Structure):

@@ -106,7 +106,27 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                 row0 = 0 if shared else h * 32             # table row of lane 0
                 rows = 32 if shared else 64
                 add = h * prm.half_add if shared else 0    # slot offset of this half
-                if g.k == 2:
+                if g.k == 2 and g.nnz:   # sparse DFMA sub-op: lane = tuple
+                    nnz = int(g.nnz)
+                    sv = dbl[g.a_off:g.a_off + 2 * nnz].reshape(nnz, 2) @ np.array([1, 1j])
+                    rs = [int(v) for v in u16[(g.a_off + 2 * nnz) * 4:(g.a_off + 2 * nnz) * 4 + 17]]
+                    assert rs[0] == 0 and rs[16] == nnz and rs == sorted(rs)
+                    rd, wr = [], []
+                    for lane in range(32):
+                        r = row0 + lane
+                        tin = [add + int(u16[g.t_off + e * rows + r]) for e in range(nnz)]
+                        tout = [add + int(u16[g.t_off + (nnz + i) * rows + r]) for i in range(16)]
+                        x = {o: st[o] for o in tin}
+                        y = np.zeros(16, dtype=np.complex128)
+                        for i in range(16):
+                            for e in range(rs[i], rs[i + 1]):
+                                y[i] += sv[e] * x[tin[e]]
+                        st[tout] = y
+                        rd += tin
+                        wr += tout
+                    if check:   # the inputs are members of the lane's own 16-member tuple
+                        assert len(set(wr)) == 512 and set(rd) <= set(wr)
+                elif g.k == 2:
                     F = dbl[g.a_off:g.a_off + 768].reshape(3, 4, 32, 2).transpose(0, 3, 1, 2)
                     a_ = F[0]
                     b_ = F[2] + F[0]

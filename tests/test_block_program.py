@@ -76,6 +76,13 @@ def _bank_degrees(prm, blob):
         if g.k != 2:
             continue
         rows = 32 if prm.half_add >= 0 else 64
+        if g.nnz:   # sparse sub-op: [nnz + 16 entries][rows] slots, one tuple per lane
+            for e in range(int(g.nnz) + 16):
+                for h in range(rows // 32):
+                    T = np.array([int(u16[g.t_off + e * rows + h * 32 + l]) for l in range(32)])
+                    for ph in range(4):
+                        worst.append(np.bincount(T[8 * ph: 8 * ph + 8] % 8, minlength=8).max())
+            continue
         for h in range(rows // 32):
             T = np.array([lane_table(u16, g.t_off, rows, h * 32 + l, 32)
                           for l in range(32)])               # [lane][32]

@@ -1346,12 +1346,16 @@ bool block_enabled() {
 }
 
 // sparse k = 2 sub-ops (DFMA, tanq_block.cu blk_sub_k2s) take superoperators with at most
-// this many nonzeros (env TANQ_SPARSE_MAX; 0 = always DMMA)
+// this many nonzeros (env TANQ_SPARSE_MAX, up to 64).  Default 0 = always DMMA: measured on
+// QPE-16 (36-40 of 256 entries nonzero in 97 of its 128 updates) the sparse form is slower,
+// 24.3 vs 15.8 ms per group pass (profiles/r02_sparse_subop_experiment.txt) -- every nonzero
+// costs a dependent table + element load from shared memory, while DMMA reads each element
+// once per k-step for 8 output rows.
 int sparse_max() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("TANQ_SPARSE_MAX");
-    v = e ? std::max(0, std::min(64, std::atoi(e))) : 64;
+    v = e ? std::max(0, std::min(64, std::atoi(e))) : 0;
   }
   return v;
 }

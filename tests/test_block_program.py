@@ -199,3 +199,50 @@ def test_block_program_four_qubit_groups(Plan, packed):
             assert np.abs(a[keep] - aref[keep]).max() < 1e-12, (cfg, qs)
             seen += 1
     assert seen >= 2
+
+
+SPARSE_SNIPPET = r"""
+import os, sys, numpy as np
+sys.path.insert(0, %(root)r); sys.path.insert(0, %(tests)r)
+import workloads as W
+from oracle import dense
+from paper_2404_13184_b200.tanq import Plan
+from _block_emu import emulate, pair_swap, phys_of_rho
+rng = np.random.default_rng(5)
+n = 7
+c, nm = W.config_workload(4, n=n)
+plan = Plan(None, c, nm, fuse=2, k_max=3)
+seen = 0
+for i, (qs, S) in enumerate(plan.ops()):
+    for packed in (True, False):
+        prog = plan.block_program(i, packed=packed)
+        if prog is None or not any(prog[0].sub[j].nnz for j in range(prog[0].n_sub)):
+            continue
+        rho = W.random_density(rng, n, rank=3)
+        a, _, _ = phys_of_rho(rho, n)
+        emulate(a, *prog)
+        ref = np.ascontiguousarray(rho.copy()); dense.apply_superop(ref, n, qs, S)
+        aref, _, _ = phys_of_rho(ref, n)
+        P = np.arange(4 ** n)
+        keep = np.array([p <= pair_swap(int(p)) for p in P]) if packed else np.ones(4 ** n, bool)
+        assert np.abs(a[keep] - aref[keep]).max() < 1e-12
+        seen += 1
+assert seen >= 4, seen
+print("OK", seen)
+"""
+
+
+def test_block_program_sparse_subops():
+    """TANQ_SPARSE_MAX=64 (read once per process: a subprocess): QPE's sparse noisy CX / CP
+    superoperators become sparse DFMA sub-ops (value list, row starts, per-lane slot tables);
+    the emulated program equals the oracle's superoperator on a random state."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TANQ_SPARSE_MAX="64")
+    r = subprocess.run([sys.executable, "-c", SPARSE_SNIPPET % {
+        "root": root, "tests": os.path.join(root, "tests")}], env=env, capture_output=True,
+        text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert r.stdout.strip().splitlines()[-1].startswith("OK")

@@ -43,18 +43,33 @@ for seed in range(4):
             rel = np.linalg.norm(d) / np.linalg.norm(ref)
             assert mx <= 1e-10 and rel <= 1e-12, (seed, kmax, mirror, mx, rel)
             worst = max(worst, mx)
+for n in (7, 9):                              # QPE: sparse noisy CX / CP superoperators
+    c, nm = W.config_workload(4, n=n)
+    ref = dense.run(c, nm)
+    N = 2 ** n
+    with Simulator(n) as sim:
+        sim.run_circuit(c, nm, fuse=2, k_max=3)
+        got = sim.get_state().reshape(N, N).T
+    mx = np.abs(got - ref).max()
+    assert mx <= 1e-10 and np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12, (n, mx)
+    worst = max(worst, mx)
 print("OK", worst)
 """
 
 
-@pytest.mark.parametrize("group,k2path,mirror", [
-    ("warp", "direct", "1"), ("q1", "tile", "1"), ("o1", "auto", "1"), ("auto", "auto", "1"),
-    ("auto", "direct", "0"), ("q1", "auto", "0"), ("warp", "tile", "0"), ("o1", "tile", "0")])
-def test_kernel_variant_parity(group, k2path, mirror):
+@pytest.mark.parametrize("group,k2path,mirror,sparse", [
+    ("warp", "direct", "1", "0"), ("q1", "tile", "1", "0"), ("o1", "auto", "1", "0"),
+    ("auto", "auto", "1", "0"), ("auto", "direct", "0", "0"), ("q1", "auto", "0", "0"),
+    ("warp", "tile", "0", "0"), ("o1", "tile", "0", "0"),
+    ("auto", "auto", "1", "64"), ("auto", "auto", "0", "64")])
+def test_kernel_variant_parity(group, k2path, mirror, sparse):
+    """sparse = 64: the block kernel's sparse DFMA sub-op (TANQ_SPARSE_MAX) for every k=2
+    sub-op with at most 64 nonzeros."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path, TANQ_MIRROR=mirror)
+    env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path, TANQ_MIRROR=mirror,
+               TANQ_SPARSE_MAX=sparse)
     r = subprocess.run([sys.executable, "-c", SNIPPET % {"root": ROOT}], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]

@@ -513,7 +513,7 @@ def run_ours(args):
                             f"peer-to-peer remap swaps (--remap p2p)" if args.remap == "p2p" else
                             f"{args.shards} virtual shards on 1 GPU (remap test mode)"),
             "plan": {"kernel_ops": st["ops_fused"],
-                     "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"]],
+                     "kernels_by_k": [st["n_k1"], st["n_k2"], st["n_k3"], st["n_k4"], st["n_k5"]],
                      "remaps_per_step": st["n_remaps"], "shard_bytes": info["shard_bytes"],
                      "plan_ms": pinfo["plan_ms"], "plan_wall_ms": plan_wall_ms,
                      "e2e_plan_ms": statistics.median(plan_ms_e2e)},

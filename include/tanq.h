@@ -130,10 +130,11 @@ typedef struct {
 } tanq_readout;
 
 /* fuse: 0 none, 1 paper (same qubit / same ordered pair), 2 greedy up to k_max
- * with the B200 cost model (default).  k_max in {1,2,3,4}: fused superoperators never exceed
+ * with the B200 cost model (default).  k_max in {1,...,5}: fused superoperators never exceed
  * 2 qubits (or a user's 3-qubit op); k_max >= 3 lets the K3 group kernel run several of them
- * in one HBM pass over 3-qubit (k_max = 3, default) or up to 4-qubit tiles (k_max = 4; slower
- * at n = 16 on B200).  chunk_bytes: reserved, must be 0 (the remap
+ * in one HBM pass over 3-qubit (k_max = 3, default) or up to 4-qubit tiles (k_max = 4), and
+ * k_max = 5 forms "block groups" of up to 5 qubits with at most 3 outside {0, 1} (the block
+ * kernel's 5-qubit shared-memory block).  chunk_bytes: reserved, must be 0 (the remap
  * staging is fixed when a multi-process handle is created: 2 x 2 pipelined slots of 128 MiB,
  * DESIGN.md §7).  flags: bit0 = record per-kernel CUDA-event timings; bit1 = plans
  * on single-shard handles capture their launches into a CUDA graph on the first
@@ -152,7 +153,7 @@ typedef struct {
   uint64_t ops_fused;      /* fused ops executed (kernel launches of the plan) */
   uint64_t gate_updates;   /* fused-gate updates: k<=2 fused superoperators applied to the whole
                               state (a K3 group of m sub-ops counts m, a dense k=3 op counts 1) */
-  uint64_t n_k[5];         /* kernels by arity k = 1..4 (index k; k = 3/4: K3 group kernels) */
+  uint64_t n_k[6];         /* kernels by arity k = 1..5 (index k; k >= 3: K3 group kernels) */
   uint64_t n_remaps;       /* global<->local bit swaps */
   uint64_t remap_bytes;    /* bytes sent by this process */
   double plan_ms;          /* host planning time */
@@ -245,10 +246,12 @@ tanq_status tanq_plan_create_host(int n_qubits, int world_size, const tanq_circu
 tanq_status tanq_plan_info(const tanq_plan* p, tanq_run_stats* st);
 /* Execution schedule of a plan on world_size shards, as the engine runs it: items of three
  * int32 {kind, x, y}; kind 0 = fused op x; kind 1 = remap swapping physical bit x (global)
- * with local bit y (A-6).  Pass items = NULL to query the count. */
+ * with local bit y (bit layout, A-6); kind 2 = parity-layout remap: half-global
+ * qubit x trades places with fully local qubit y.  Pass items = NULL to query
+ * the count. */
 tanq_status tanq_plan_schedule(const tanq_plan* p, int world_size, int32_t* items, uint64_t max,
                                uint64_t* n_items);
-/* Fused op i: arity k (<= 4), qubits (k ints) and, if S != NULL, its 4^k x 4^k superoperator
+/* Fused op i: arity k (<= 5), qubits (k ints) and, if S != NULL, its 4^k x 4^k superoperator
  * in the paper's vec convention (local index r + c 2^k over qubits[0..k-1]).  For a K3 group
  * this is the product of its sub-ops. */
 tanq_status tanq_plan_get_op(const tanq_plan* p, uint64_t i, int* k, int* qubits, tanq_c64* S);

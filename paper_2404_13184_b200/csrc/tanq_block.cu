@@ -512,11 +512,12 @@ __global__ void __launch_bounds__(384, 1)
       if (!first && nxt < nb) issue(nxt, s ^ 1);
     }
     if (!(p.dbg & 1)) {
-      const bool shared_tab = p.half_add >= 0;
-      double2* Xh = X + (shared_tab ? half * p.half_add : 0);
-      const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
+        if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
+        const bool shared_tab = g.hadd >= 0;
+        double2* Xh = X + (shared_tab ? half * g.hadd : 0);
+        const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2 && g.nnz)
@@ -684,6 +685,7 @@ __global__ void __launch_bounds__(384, 1)
       const int trow = half * 32 + lane;
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
+        if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
         const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2 && g.nnz)

@@ -282,7 +282,7 @@ bool is_herm_preserving(const Mat& S, int k) {
 // ------------------------------------------------------------------------------------
 struct FusedOp {
   int k = 0;
-  int q[4] = {0, 0, 0, 0};  // k <= 3 for ops; a factored group may span 4 qubits
+  int q[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // k <= 3 for ops; a factored group spans <= 5 qubits
   Mat S;            // 4^k, local index over q[0..k-1] (for a factored group: the dense product)
   int parts = 1;    // number of pre-fusion ops folded in
   bool herm = true;  // Hermiticity-preserving: S[(r',c'),(r,c)] = conj S[(c',r'),(c,r)]
@@ -335,6 +335,31 @@ FusedOp merge(const FusedOp& Q, const FusedOp& G) {
 // is the group + the lowest free qubit, and its lowest 4 bits must be qubits 0 and 1 for
 // 256 B contiguous pieces); other 4-qubit unions stay 3-qubit groups.  Env TANQ_QUAD_ANY=1
 // allows any 4-qubit group (round-1 behaviour: those run on the cooperative tile kernel).
+// k_max = 5 ("block groups"): a factored group may span up to 5 qubits when at most 3 of them
+// are outside {0, 1} -- the block kernel's 5-qubit block always holds qubits 0 and 1 (its
+// contiguous pieces), so sub-ops on any block qubit ride in the same HBM pass.  Members per
+// block group are capped (env TANQ_BLOCK_GROUP_MAX, default 6): every k=2 sub-op adds ~10 KB
+// of fragments and tables to the shared-memory blob, which costs warp pairs.
+int block_group_max() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("TANQ_BLOCK_GROUP_MAX");
+    v = e ? std::max(2, std::min(12, std::atoi(e))) : 6;
+  }
+  return v;
+}
+bool block_group_fits(const int* q, int k) {
+  static int hmax = -1;
+  if (hmax < 0) {
+    const char* e = std::getenv("TANQ_BLOCK_HIGH_MAX");  // planner experiments only: the
+    hmax = e ? std::max(1, std::min(3, std::atoi(e))) : 3;  // block kernel holds 3 + {0, 1}
+  }
+  if (k > hmax + 2) return false;
+  int high = 0;
+  for (int i = 0; i < k; ++i) high += q[i] >= 2 ? 1 : 0;
+  return high <= hmax;
+}
+
 bool quad_ok(const int* q) {
   static int any = -1;
   if (any < 0) {
@@ -390,7 +415,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
   if (mode == 1) return pass(in, 2, true);
   std::vector<FusedOp> l1 = pass(in, std::min(kmax, 2), false);
   if (kmax < 3) return l1;
-  const int glim = std::min(kmax, 4);  // group qubits: 3, or 4 (factored groups only)
+  const int glim = kmax == 5 ? 8 : std::min(kmax, 4);  // group qubits (factored groups only)
   // 3-qubit grouping: greedy groups of <= 3 qubits over the k<=2 ops; a group replaces its
   // members only when their summed pass cost exceeds one dense k=3 pass.
   struct Group {
@@ -411,7 +436,7 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
       bool has3 = G.k == 3;
       for (int m : Q.members) has3 |= l1[m].k == 3;
       const int lim = has3 ? 3 : glim;  // dense k=3 sub-ops only run on 3-qubit tiles
-      int uq[4], uk = Q.op.k;
+      int uq[8], uk = Q.op.k;
       for (int i = 0; i < Q.op.k; ++i) uq[i] = Q.op.q[i];
       bool fits = true;
       for (int j = 0; j < G.k && fits; ++j) {
@@ -422,7 +447,13 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
         }
       }
       if (uk > lim) fits = false;  // a dense k=3 op never joins a 4-qubit group
-      if (fits && uk == 4 && !quad_ok(uq)) fits = false;
+      if (kmax == 5) {
+        if (fits && uk >= 4 && (!block_group_fits(uq, uk) ||
+                                (int)Q.members.size() + 1 > block_group_max()))
+          fits = false;
+      } else if (fits && uk == 4 && !quad_ok(uq)) {
+        fits = false;
+      }
       if (fits) {
         Q.op.k = uk;
         for (int i = 0; i < uk; ++i) Q.op.q[i] = uq[i];
@@ -457,14 +488,18 @@ std::vector<FusedOp> fuse(const std::vector<FusedOp>& in, int mode, int kmax) {
       for (int m : A.members) has3 |= l1[m].k == 3;
       for (int m : B.members) has3 |= l1[m].k == 3;
       const int lim = has3 ? 3 : glim;
-      int uq[8], uk = B.op.k;
+      int uq[16], uk = B.op.k;
       for (int t = 0; t < B.op.k; ++t) uq[t] = B.op.q[t];
       for (int t = 0; t < A.op.k; ++t) {
         bool f = false;
         for (int u = 0; u < uk; ++u) f |= uq[u] == A.op.q[t];
         if (!f) uq[uk++] = A.op.q[t];
       }
-      if (uk <= lim && uk >= 3 && (uk < 4 || quad_ok(uq))) {  // (k <= 2 unions: level 1)
+      const bool ok4 = kmax == 5 ? (uk < 4 || (block_group_fits(uq, uk) &&
+                                               (int)(A.members.size() + B.members.size()) <=
+                                                   block_group_max()))
+                                 : (uk < 4 || quad_ok(uq));
+      if (uk <= lim && uk >= 3 && ok4) {  // (k <= 2 unions: level 1)
         B.op.k = uk;
         for (int t = 0; t < uk; ++t) B.op.q[t] = uq[t];
         B.members.insert(B.members.begin(), A.members.begin(), A.members.end());
@@ -1395,10 +1430,10 @@ bool block_k2_enabled() {
 bool block_ok(const tanq_sim* s, const FusedOp& op) {
   if (!block_enabled() || s->L < 12) return false;
   if (op.k == 2 && op.sub.empty()) return block_k2_enabled() && k2_tiled(s, op);
-  if (op.k == 4) {  // 4-qubit groups: the block's lowest 4 bits must be physical 0..3
-    if (op.sub.empty()) return false;
+  if (op.k == 4 || op.k == 5) {  // 4- / 5-qubit groups: the block's lowest 4 bits must be
+    if (op.sub.empty()) return false;  // physical 0..3
     std::vector<int> pos;
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < op.k; ++j)
       for (int b = 0; b < 2; ++b) pos.push_back((int)s->phys[2 * op.q[j] + b]);
     for (int f = 0; pos.size() < 10; ++f)
       if (std::find(pos.begin(), pos.end(), f) == pos.end()) pos.push_back(f);
@@ -1560,9 +1595,22 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       for (int e = 0; e < 256; ++e) snz[i][e] = (Sm[e].x != 0.0 || Sm[e].y != 0.0) ? 1 : 0;
     }
     for (int t = 0; t < 2 * subs[i]->k; ++t) smem_bits[i].push_back(bit_of_pos(smap[i].bits[t].first));
+  }
+  // warp-half bit of each sub-op: the group's highest tuple bit; a 5-qubit block group has
+  // none, so each sub-op splits the block on a bit it does not touch (in-piece bit 3 when
+  // possible: one shared table), and the pair meets at a barrier when the split changes
+  std::vector<int> shalf(subs.size(), half);
+  for (size_t i = 0; i < subs.size(); ++i) {
+    auto in_sub = [&](int j) {
+      return std::find(smem_bits[i].begin(), smem_bits[i].end(), j) != smem_bits[i].end();
+    };
+    if (shalf[i] < 0) {
+      if (!in_sub(3)) shalf[i] = 3;
+      for (int j = 9; j >= 0 && shalf[i] < 0; --j)
+        if (!in_sub(j)) shalf[i] = j;
+    }
     for (int j = 0; j < 10; ++j)
-      if (j != half && std::find(smem_bits[i].begin(), smem_bits[i].end(), j) == smem_bits[i].end())
-        scol_bits[i].push_back(j);
+      if (j != shalf[i] && !in_sub(j)) scol_bits[i].push_back(j);
   }
   // piece-placement weights: start from one rotation per qubit pair of piece-index bits,
   // (1,2), (4,1), (2,4) (conflict-free for every pair of 3 group qubits when the group sits
@@ -1750,15 +1798,18 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
   p.dbg = (uint32_t)dbg;
   p.n_sub = (int)subs.size();
   // the warp-half bit is in-piece bit 3 (both halves' offsets differ by 8 units): one table
-  const bool share = half == 3 && !use_tma;
-  const int halves = share ? 1 : 2;
-  p.half_add = share ? 8 : -1;
+  p.half_add = (shalf[0] == 3 && !use_tma) ? 8 : -1;
   // blob: per sub-op fragments then tables (both 16 B aligned)
   size_t off = 0;
   for (size_t i = 0; i < subs.size(); ++i) {
     const FusedOp& sb = *subs[i];
     tanq::BlockSub& g = p.sub[i];
     g.k = sb.k;
+    const int half = shalf[i];
+    const bool share = half == 3 && !use_tma;
+    const int halves = share ? 1 : 2;
+    g.hadd = share ? 8 : -1;
+    g.sync = (i > 0 && shalf[i] != shalf[i - 1]) ? 1 : 0;
     const BlockSubChoice ch = best_choice(sb.k, smem_bits[i], scol_bits[i], w,
                                           snz[i].empty() ? nullptr : snz[i].data());
     g.tmask = sb.k == 2 ? (int)ch.tmask : 0xff;
@@ -2049,8 +2100,31 @@ tanq_status ensure_frag_capacity(tanq_sim* s, DevScratch& d, size_t elems) {
   return TANQ_OK;
 }
 
+// 5-qubit block groups (k_max = 5) run only on the block kernel; where it cannot take one (a
+// multi-shard layout, a small register, a group whose qubits do not cover physical bits 0..3)
+// the group's sub-ops run as separate ops -- the same product, one pass each.
+const std::vector<FusedOp>& runnable_ops(const tanq_sim* s, const std::vector<FusedOp>& ops,
+                                         std::vector<FusedOp>& storage) {
+  auto needs = [&](const FusedOp& op) {
+    return op.k == 5 && (s->shards.size() != 1 || s->par || !block_ok(s, op));
+  };
+  bool any = false;
+  for (const auto& op : ops) any |= needs(op);
+  if (!any) return ops;
+  storage.clear();
+  for (const auto& op : ops) {
+    if (needs(op))
+      storage.insert(storage.end(), op.sub.begin(), op.sub.end());
+    else
+      storage.push_back(op);
+  }
+  return storage;
+}
+
 // Execute a list of fused ops in order (remaps inserted as needed).
-tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops) {
+tanq_status exec_ops(tanq_sim* s, const std::vector<FusedOp>& ops_in) {
+  std::vector<FusedOp> expanded;
+  const std::vector<FusedOp>& ops = runnable_ops(s, ops_in, expanded);
   // K3 group programs depend on the layout at execution time, so they are built op by op
   // into a persistent pinned host buffer and copied (async) to each device before the launch.
   size_t total = 0;
@@ -2709,6 +2783,8 @@ namespace {
 tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
   Shard& sh = s->shards[0];
   auto& g = p->g;
+  std::vector<FusedOp> expanded;
+  const std::vector<FusedOp>& ops = runnable_ops(s, p->ops, expanded);
   const bool hit = g.exec && g.sim == s && g.data == sh.data && g.herm == s->herm_state &&
                    g.mirror == s->mirror_allowed && g.packed == s->packed &&
                    std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0;
@@ -2725,7 +2801,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
       CUDA_TRY(cudaSetDevice(sh.device));
     }
     size_t total = 0;
-    for (const auto& op : p->ops)
+    for (const auto& op : ops)
       if (op.k >= 2) total += prog_capacity(op);  // upper bound (k = 2 may run direct)
     std::vector<double2> host(total ? total : 1);
     std::vector<tanq::GroupParams> gps;
@@ -2734,7 +2810,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     std::vector<int> kind;  // per op: 0 direct, 1 group, 2 block
     size_t off = 0;
     const bool herm_in = s->herm_state;
-    for (const auto& op : p->ops) {  // the Hermitian flag as it will be when op runs
+    for (const auto& op : ops) {  // the Hermitian flag as it will be when op runs
       if (block_ok(s, op)) {
         bps.emplace_back();
         const size_t e = (build_block(s, op, bps.back(), reinterpret_cast<unsigned char*>(
@@ -2771,8 +2847,8 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
     off = 0;
     size_t gi = 0, bi = 0;
     tanq_status st = TANQ_OK;
-    for (size_t oi = 0; oi < p->ops.size(); ++oi) {
-      const FusedOp& op = p->ops[oi];
+    for (size_t oi = 0; oi < ops.size(); ++oi) {
+      const FusedOp& op = ops[oi];
       if (kind[oi] == 0) {
         st = launch_op(s, op, nullptr, nullptr);
       } else {
@@ -2805,7 +2881,7 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
   CUDA_TRY(cudaGraphLaunch(g.exec, sh.stream));
   s->launches += g.kernels;
   s->packed = g.packed_end;
-  for (const auto& op : p->ops)
+  for (const auto& op : ops)
     if (!op.herm) s->herm_state = false;
   return TANQ_OK;
 }
@@ -2821,7 +2897,8 @@ static tanq_status plan_create(int n, int L, const tanq_circuit* c, const tanq_n
   tanq_run_opts opts{2, 3, 0, 0, 0};
   if (o) opts = *o;
   if (opts.fuse < 0 || opts.fuse > 2) return fail(TANQ_E_ARG, "fuse must be 0, 1 or 2");
-  if (opts.k_max < 1 || opts.k_max > 4) return fail(TANQ_E_ARG, "k_max must be 1..4");
+  if (opts.k_max < 1 || opts.k_max > 5) return fail(TANQ_E_ARG, "k_max must be 1..5");
+  if (opts.k_max == 5 && L < 14) opts.k_max = 4;  // 5-qubit block groups need block tuples
   if (opts.k_max == 4 && L < 10) opts.k_max = 3;  // 4-qubit tiles need 8 member bits + tuples
   if (opts.k_max == 3 && L < 6) opts.k_max = 2;
   const auto t0 = std::chrono::steady_clock::now();

@@ -64,6 +64,10 @@ struct BlockSub {
                    // sparse k=2: [nnz + 16][rows] (entry inputs, then the 16 outputs)
   int32_t tmask;   // k=2: nonzero 8x4 A tiles, bit mt * 4 + ks (zero tiles are skipped)
   int32_t nnz;     // k=2: > 0 -> sparse DFMA sub-op (one tuple per lane), 0 -> DMMA
+  int32_t hadd;    // >= 0: one table for both warp halves, the second adding hadd units;
+                   // -1: a table per half (the warp-half bit of this sub-op)
+  int32_t sync;    // 1: the warp-half bit differs from the previous sub-op's (5-qubit block
+                   // groups): the pair meets at a barrier first
 };
 struct BlockParams {
   const void* blob;          // sub-op fragments + offset tables (device), copied to shared

@@ -65,21 +65,22 @@ class tanq_run_opts(ctypes.Structure):
 
 class tanq_run_stats(ctypes.Structure):
     _fields_ = [("ops_in", ctypes.c_uint64), ("ops_fused", ctypes.c_uint64),
-                ("gate_updates", ctypes.c_uint64), ("n_k", ctypes.c_uint64 * 5), ("n_remaps", ctypes.c_uint64),
+                ("gate_updates", ctypes.c_uint64), ("n_k", ctypes.c_uint64 * 6), ("n_remaps", ctypes.c_uint64),
                 ("remap_bytes", ctypes.c_uint64), ("plan_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {"ops_in": self.ops_in, "ops_fused": self.ops_fused,
                 "gate_updates": self.gate_updates,
                 "n_k1": self.n_k[1], "n_k2": self.n_k[2], "n_k3": self.n_k[3],
-                "n_k4": self.n_k[4],
+                "n_k4": self.n_k[4], "n_k5": self.n_k[5],
                 "n_remaps": self.n_remaps, "remap_bytes": self.remap_bytes,
                 "plan_ms": self.plan_ms}
 
 
 class tanq_block_sub(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("a_off", ctypes.c_int32), ("t_off", ctypes.c_int32),
-                ("tmask", ctypes.c_int32), ("nnz", ctypes.c_int32)]
+                ("tmask", ctypes.c_int32), ("nnz", ctypes.c_int32), ("hadd", ctypes.c_int32),
+                ("sync", ctypes.c_int32)]
 
 
 class tanq_block_params(ctypes.Structure):
@@ -307,18 +308,19 @@ class Plan:
                                         ctypes.byref(n)), "tanq_plan_schedule")
         return [tuple(int(v) for v in items[3 * i:3 * i + 3]) for i in range(n.value)]
 
+    def op(self, i: int):
+        """(qubits tuple, S ndarray 4^k x 4^k) of fused op i (a group: its sub-ops' product)."""
+        k = ctypes.c_int()
+        q = (ctypes.c_int * 8)()
+        _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, None), "tanq_plan_get_op")
+        S = np.empty((4 ** k.value, 4 ** k.value), dtype=np.complex128)
+        _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, S.ctypes.data),
+               "tanq_plan_get_op")
+        return tuple(q[:k.value]), S
+
     def ops(self):
         """[(qubits tuple, S ndarray 4^k x 4^k)] of the fused plan."""
-        out = []
-        for i in range(self.info()["ops_fused"]):
-            k = ctypes.c_int()
-            q = (ctypes.c_int * 4)()
-            _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, None), "tanq_plan_get_op")
-            S = np.empty((4 ** k.value, 4 ** k.value), dtype=np.complex128)
-            _check(lib().tanq_plan_get_op(self.h, i, ctypes.byref(k), q, S.ctypes.data),
-                   "tanq_plan_get_op")
-            out.append((tuple(q[:k.value]), S))
-        return out
+        return [self.op(i) for i in range(self.info()["ops_fused"])]
 
     def block_program(self, i: int, packed: bool = True):
         """(params, blob bytes) of the block-pipeline kernel for op i, or None."""

@@ -102,10 +102,10 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
         for q in range(int(prm.n_sub)):
             g = prm.sub[q]
             for h in range(2):
-                shared = prm.half_add >= 0
+                shared = g.hadd >= 0                        # per sub-op warp-half bit
                 row0 = 0 if shared else h * 32             # table row of lane 0
                 rows = 32 if shared else 64
-                add = h * prm.half_add if shared else 0    # slot offset of this half
+                add = h * g.hadd if shared else 0          # slot offset of this half
                 if g.k == 2 and g.nnz:   # sparse DFMA sub-op: lane = tuple
                     nnz = int(g.nnz)
                     sv = dbl[g.a_off:g.a_off + 2 * nnz].reshape(nnz, 2) @ np.array([1, 1j])

@@ -75,7 +75,7 @@ def _bank_degrees(prm, blob):
         g = prm.sub[q]
         if g.k != 2:
             continue
-        rows = 32 if prm.half_add >= 0 else 64
+        rows = 32 if g.hadd >= 0 else 64
         if g.nnz:   # sparse sub-op: [nnz + 16 entries][rows] slots, one tuple per lane
             for e in range(int(g.nnz) + 16):
                 for h in range(rows // 32):
@@ -246,3 +246,49 @@ def test_block_program_sparse_subops():
         text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert r.stdout.strip().splitlines()[-1].startswith("OK")
+
+
+@pytest.mark.parametrize("packed", [True, False])
+@pytest.mark.parametrize("case", ["qpe", "layered", "random"])
+def test_block_groups_kmax5_circuit(Plan, case, packed):
+    """k_max = 5 block groups (up to 5 qubits, at most 3 outside {0, 1}; each sub-op splits the
+    block on its own warp-half bit, with a pair barrier where the split changes): the whole
+    plan -- block programs through the emulator, other ops through the oracle -- must equal
+    the oracle's run of the circuit."""
+    n = 7
+    if case == "qpe":
+        c, nm = W.config_workload(4, n=n)
+    elif case == "layered":
+        c, nm = W.config_workload(3, n=n, depth=14)
+    else:
+        c = W.random_circuit(n, 70, seed=5300, kmax=2, allow_matrix=True)
+        nm = W.synthetic_calibration(c, 3, depol=True, thermal=True, overrot=True)
+    plan = Plan(None, c, nm, fuse=2, k_max=5)
+    info = plan.info()
+    assert info["n_k5"] > 0, info
+    N = 2 ** n
+    rho = dense.ground(n)
+    a, P_r, P_c = phys_of_rho(rho, n)
+    P = np.arange(N * N)
+    noncanon = np.array([p > pair_swap(int(p)) for p in P])
+    syncs = 0
+    for i in range(info["ops_fused"]):
+        prog = plan.block_program(i, packed=packed)
+        if prog is not None:
+            prm, blob = prog
+            syncs += sum(int(prm.sub[j].sync) for j in range(prm.n_sub))
+            emulate(a, prm, blob)
+            continue
+        if packed:   # restore the stale half before a full-layout op
+            a[noncanon] = np.conj(a[np.array([pair_swap(int(p)) for p in P[noncanon]])])
+        qs, S = plan.op(i)
+        r = a[(P_r[:, None] | P_c[None, :]).reshape(-1)].reshape(N, N)
+        r = np.ascontiguousarray(r)
+        dense.apply_superop(r, n, qs, S)
+        a[(P_r[:, None] | P_c[None, :]).reshape(-1)] = r.reshape(-1)
+    if packed:
+        a[noncanon] = np.conj(a[np.array([pair_swap(int(p)) for p in P[noncanon]])])
+    got = a[(P_r[:, None] | P_c[None, :]).reshape(-1)].reshape(N, N)
+    ref = dense.run(c, nm)
+    assert np.abs(got - ref).max() < 1e-12
+    assert syncs > 0   # some block group changed its warp-half bit between sub-ops

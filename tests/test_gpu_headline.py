@@ -138,9 +138,9 @@ for n in (7, 8, 9):
     nm = W.synthetic_calibration(c, n, depol=True, thermal=True, overrot=True)
     ref = dense.run(c, nm)
     N = 2 ** n
-    for kmax in (3, 4):
-        assert Plan(None, c, nm, fuse=2, k_max=kmax).info()["n_k3"] + \
-            Plan(None, c, nm, fuse=2, k_max=kmax).info()["n_k4"] > 0
+    for kmax in (3, 4, 5):
+        inf = Plan(None, c, nm, fuse=2, k_max=kmax).info()
+        assert inf["n_k3"] + inf["n_k4"] + inf["n_k5"] > 0
         with Simulator(n) as sim:
             sim.run_circuit(c, nm, fuse=2, k_max=kmax)
             p = sim.probs()
@@ -190,3 +190,22 @@ def test_qpe16_prefix_bench_plan_vs_oracle(Sim):
         assert st["n_k3"] == info["n_k3"]
         mx, rel = _full_compare(sim, ref, 16)
     assert mx <= ABS and rel <= REL, (mx, rel)
+
+
+@pytest.mark.parametrize("config,n", [(4, 9), (3, 9), (4, 10), (2, 10)])
+def test_block_groups_kmax5(Sim, config, n):
+    """k_max = 5: block groups of up to 5 qubits (at most 3 outside {0, 1}) on the block
+    kernel, each sub-op with its own warp-half split, packed and full layouts."""
+    from paper_2404_13184_b200.tanq import Plan
+    c, nm = W.config_workload(config, n=n, **({"depth": 20} if config == 3 else {}))
+    assert Plan(None, c, nm, fuse=2, k_max=5).info()["n_k5"] > 0
+    ref = dense.run(c, nm)
+    N = 2 ** n
+    for mirror in (True, False):
+        with Sim(n) as sim:
+            sim.run_circuit(c, nm, fuse=2, k_max=5, mirror=mirror)
+            p = sim.probs(dense.readout_of(nm))
+            got = sim.get_state().reshape(N, N).T
+        np.testing.assert_allclose(p, dense.probs(ref, n, dense.readout_of(nm)), atol=ABS)
+        d = got - ref
+        assert np.abs(d).max() <= ABS and np.linalg.norm(d) / np.linalg.norm(ref) <= REL

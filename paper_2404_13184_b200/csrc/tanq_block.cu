@@ -345,6 +345,94 @@ __device__ __forceinline__ void blk_sub_k2s(double2* X, const double* F, const u
   for (int i = 0; i < 16; ++i) X[To[i * rows]] = y[i];
 }
 
+// Real-basis transform (BlockParams::rb_nq): per group qubit, every (x1, x2) = (row 1 col 0,
+// row 0 col 1) element pair of the block -> (x1 + x2, i (x2 - x1)) (forward) or back,
+// x1 = (u1 + i u2) / 2, x2 = (u1 - i u2) / 2.  Each pair thread owns 4 pairs per qubit
+// (table T: [nq][64][4][2] slots); the pair meets at a barrier before every qubit's pass
+// (and, forward, after the last) because the pairs of one qubit span both warp halves.
+__device__ __forceinline__ void blk_rbasis(double2* X, const uint16_t* T, int nq, int pt, int pair,
+                                           bool fwd) {
+  for (int t = 0; t < nq; ++t) {
+    pair_bar(pair);
+    const uint4 e = reinterpret_cast<const uint4*>(T)[t * 64 + pt];
+    const uint32_t w[4] = {e.x, e.y, e.z, e.w};
+    double2 u[4], v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u[j] = X[w[j] & 0xffffu];
+      v[j] = X[w[j] >> 16];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 a = u[j], b = v[j];
+      if (fwd) {
+        X[w[j] & 0xffffu] = make_double2(a.x + b.x, a.y + b.y);
+        X[w[j] >> 16] = make_double2(a.y - b.y, b.x - a.x);
+      } else {
+        X[w[j] & 0xffffu] = make_double2(0.5 * (a.x - b.y), 0.5 * (a.y + b.x));
+        X[w[j] >> 16] = make_double2(0.5 * (a.x + b.y), 0.5 * (a.y - b.x));
+      }
+    }
+  }
+  if (fwd && nq) pair_bar(pair);
+}
+
+// k = 2 sub-op in the real basis: Y = R X with R real, i.e. two real products per n-tile
+// (Re y = R Re x, Im y = R Im x) -- 2/3 of the DMMAs of the complex form and no B-side adds.
+// F: [4 ks][32 lanes][2 mt] doubles; T: the same offset tables as blk_sub_k2.
+__device__ __forceinline__ void blk_sub_k2r(double2* X, const double* F, const uint16_t* T,
+                                            int lane, int trow, int rows) {
+  double ar[2][4];
+  const double2* F2 = reinterpret_cast<const double2*>(F);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const double2 v = F2[ks * 32 + lane];
+    ar[0][ks] = v.x;
+    ar[1][ks] = v.y;
+  }
+  uint32_t ob[8], od[8];
+  {
+    const uint4* t4 = reinterpret_cast<const uint4*>(T);
+    const uint4 b0 = t4[trow], b1 = t4[rows + trow], d0 = t4[2 * rows + trow],
+                d1 = t4[3 * rows + trow];
+    ob[0] = b0.x; ob[1] = b0.y; ob[2] = b0.z; ob[3] = b0.w;
+    ob[4] = b1.x; ob[5] = b1.y; ob[6] = b1.z; ob[7] = b1.w;
+    od[0] = d0.x; od[1] = d0.y; od[2] = d0.z; od[3] = d0.w;
+    od[4] = d1.x; od[5] = d1.y; od[6] = d1.z; od[7] = d1.w;
+  }
+  auto boff = [&](int ks, int j) {
+    const int e = ks * 4 + j;
+    return (int)((ob[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+  };
+  auto doff = [&](int mt, int j, int c) {
+    const int e = (mt * 4 + j) * 2 + c;
+    return (int)((od[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+  };
+  double yr[4][2][2], yi[4][2][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) yr[u][mt][0] = yr[u][mt][1] = yi[u][mt][0] = yi[u][mt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 xb = X[boff(ks, u)];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        dmma(yr[u][mt][0], yr[u][mt][1], ar[mt][ks], xb.x);
+        dmma(yi[u][mt][0], yi[u][mt][1], ar[mt][ks], xb.y);
+      }
+    }
+  __syncwarp();  // every lane's B loads precede any lane's D stores
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) X[doff(mt, u, c)] = make_double2(yr[u][mt][c], yi[u][mt][c]);
+}
+
 // k = 1 sub-op (4x4 complex, DFMA): T = this lane's 16 offsets [j column][i member].
 __device__ __forceinline__ void blk_sub_k1(double2* X, const double* F, const uint16_t* T,
                                            int trow, int rows) {
@@ -512,6 +600,8 @@ __global__ void __launch_bounds__(384, 1)
       if (!first && nxt < nb) issue(nxt, s ^ 1);
     }
     if (!(p.dbg & 1)) {
+      const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
+      blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
         if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
@@ -522,12 +612,15 @@ __global__ void __launch_bounds__(384, 1)
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2 && g.nnz)
           blk_sub_k2s(Xh, F, T, trow, trows, g.nnz);
+        else if (g.k == 2 && p.rb_nq)
+          blk_sub_k2r(Xh, F, T, lane, trow, trows);
         else if (g.k == 2)
           blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
         else
           blk_sub_k1(Xh, F, T, trow, trows);
         __syncwarp();
       }
+      blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
     }
     pair_bar(pair);
     if (trp) piece_transpose(X + sstart, rot);
@@ -683,6 +776,8 @@ __global__ void __launch_bounds__(384, 1)
     if (!(p.dbg & 1)) {
       double2* Xh = X;
       const int trow = half * 32 + lane;
+      const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
+      blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
       for (int q = 0; q < p.n_sub; ++q) {
         const BlockSub& g = p.sub[q];
         if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
@@ -690,12 +785,15 @@ __global__ void __launch_bounds__(384, 1)
         const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
         if (g.k == 2 && g.nnz)
           blk_sub_k2s(Xh, F, T, trow, 64, g.nnz);
+        else if (g.k == 2 && p.rb_nq)
+          blk_sub_k2r(Xh, F, T, lane, trow, 64);
         else if (g.k == 2)
           blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, 64);
         else
           blk_sub_k1(Xh, F, T, trow, 64);
         __syncwarp();
       }
+      blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
     }
     if (kd == 0) fence_async_smem();
     pair_bar(pair);

@@ -1400,8 +1400,8 @@ size_t block_sub_bytes(int k) {
                 : 32 * 8 + 2 * 32 * 16 * 2;
 }
 
-size_t block_blob_bytes(const FusedOp& op) {  // upper bound (incl. the TMA slot table)
-  size_t b = 2048;
+size_t block_blob_bytes(const FusedOp& op) {  // upper bound (incl. TMA slot + transform tables)
+  size_t b = 2048 + 5 * 1024;
   if (op.sub.empty()) return b + block_sub_bytes(op.k);
   for (const auto& sb : op.sub) b += block_sub_bytes(sb.k);
   return b;
@@ -1562,6 +1562,47 @@ BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector
 
 // Build the block-kernel parameters and blob (fragments + offset tables) of a 3-qubit group for
 // the current layout.  Returns the blob size in bytes (written to `blob`).
+// Real basis for the block kernel (BlockParams::rb_nq).  A Hermiticity-
+// preserving superoperator commutes with J: (J x)[(r, c)] = conj x[(c, r)], so in the basis in
+// which J-invariant vectors have real coordinates -- per qubit e00, e10 + e01, i (e01 - e10),
+// e11 -- it is a real matrix R = F S F^-1.  Groups whose sub-ops are all Hermiticity-preserving
+// transform the block once after the load and back before the store; every k=2 sub-op then
+// needs 2 real DMMA products instead of 3.  Env TANQ_RBASIS=0 disables; groups with fewer
+// than TANQ_RBASIS_MIN (default 1) k=2 sub-ops stay complex.
+int rbasis_min() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = std::getenv("TANQ_RBASIS");
+    const char* m = std::getenv("TANQ_RBASIS_MIN");
+    v = (e && e[0] == '0') ? -1 : (m ? std::max(1, std::atoi(m)) : 1);
+  }
+  return v;
+}
+
+// F (forward transform) in a sub-op's member order: member bit rbit[j] / cbit[j] = row / col
+// bit of sub-op qubit j.  Pair (x1: r=1 c=0, x2: r=0 c=1) -> (u1, u2) = (x1 + x2, i (x2 - x1)).
+Mat rbasis_matrix(int k, const int* rbit, const int* cbit, bool inverse) {
+  const int M = 1 << (2 * k);
+  Mat F = identity(M);
+  for (int j = 0; j < k; ++j) {
+    Mat Fj = identity(M);
+    for (int m = 0; m < M; ++m) {
+      const int r = (m >> rbit[j]) & 1, c = (m >> cbit[j]) & 1;
+      if (!(r == 1 && c == 0)) continue;
+      const int m1 = m, m2 = (m & ~(1 << rbit[j])) | (1 << cbit[j]);
+      if (!inverse) {
+        Fj(m1, m1) = 1.0; Fj(m1, m2) = 1.0;
+        Fj(m2, m1) = cd(0, -1); Fj(m2, m2) = cd(0, 1);
+      } else {
+        Fj(m1, m1) = 0.5; Fj(m1, m2) = cd(0, 0.5);
+        Fj(m2, m1) = 0.5; Fj(m2, m2) = cd(0, -0.5);
+      }
+    }
+    F = matmul(Fj, F);
+  }
+  return F;
+}
+
 size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, unsigned char* blob) {
   const int NQ = op.k, MB = 2 * NQ;
   const MemberMap tile = member_map(s, NQ, op.q);  // group member bit u <-> tile.bits[u].first
@@ -1611,6 +1652,42 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     }
     for (int j = 0; j < 10; ++j)
       if (j != shalf[i] && !in_sub(j)) scol_bits[i].push_back(j);
+  }
+  // real basis: every sub-op Hermiticity-preserving, enough k=2 sub-ops, R real to rounding
+  std::vector<std::vector<double2>> sR(subs.size());  // sub-op matrices in the real basis
+  bool rb = false;
+  {
+    int n2 = 0;
+    bool herm = true;
+    for (const FusedOp* sb : subs) {
+      n2 += sb->k == 2 ? 1 : 0;
+      herm = herm && sb->herm;
+    }
+    rb = rbasis_min() > 0 && herm && n2 >= rbasis_min() && sparse_max() == 0;
+    for (size_t i = 0; rb && i < subs.size(); ++i) {
+      const int k = subs[i]->k, M = 1 << (2 * k);
+      int rbit[2], cbit[2];
+      for (int t = 0; t < 2 * k; ++t) {
+        const int b = smap[i].bits[t].second;  // paper-index bit: row of qubit b, col of b - k
+        if (b < k) rbit[b] = t; else cbit[b - k] = t;
+      }
+      const std::vector<double2> Sm = member_order_S(*subs[i], smap[i]);
+      Mat S(M);
+      for (int e = 0; e < M * M; ++e) S.a[e] = cd(Sm[e].x, Sm[e].y);
+      const Mat R = matmul(rbasis_matrix(k, rbit, cbit, false),
+                           matmul(S, rbasis_matrix(k, rbit, cbit, true)));
+      double mx = 0.0, im = 0.0;
+      for (const cd& v : R.a) {
+        mx = std::max(mx, std::abs(v));
+        im = std::max(im, std::abs(v.imag()));
+      }
+      if (im > 1e-13 * std::max(1.0, mx)) {
+        rb = false;
+        break;
+      }
+      sR[i].resize((size_t)M * M);
+      for (int e = 0; e < M * M; ++e) sR[i][e] = make_double2(R.a[e].real(), 0.0);
+    }
   }
   // piece-placement weights: start from one rotation per qubit pair of piece-index bits,
   // (1,2), (4,1), (2,4) (conflict-free for every pair of 3 group qubits when the group sits
@@ -1813,7 +1890,7 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
     const BlockSubChoice ch = best_choice(sb.k, smem_bits[i], scol_bits[i], w,
                                           snz[i].empty() ? nullptr : snz[i].data());
     g.tmask = sb.k == 2 ? (int)ch.tmask : 0xff;
-    const std::vector<double2> Sm = member_order_S(sb, smap[i]);  // sub-op member order
+    const std::vector<double2> Sm = rb ? sR[i] : member_order_S(sb, smap[i]);  // member order
     // sub-op member bit t <-> block bit smem_bits[i][t]
     auto sub_member = [&](const int* blkbits, int nb, int v) {  // value over blkbits -> member
       int m = 0;
@@ -1919,10 +1996,12 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
             const double2 v = Sm[(size_t)sub_member(out_bits, 4, row) * 16 + sub_member(in_bits, 4, colk)];
             const int e = (ks * 32 + lane) * 2 + mt;  // [mat][ks][lane][mt]
             F[0 * 256 + e] = v.x;
-            F[1 * 256 + e] = -(v.x + v.y);
-            F[2 * 256 + e] = v.y - v.x;
+            if (!rb) {
+              F[1 * 256 + e] = -(v.x + v.y);
+              F[2 * 256 + e] = v.y - v.x;
+            }
           }
-      off += 768 * 8;
+      off += (rb ? 256 : 768) * 8;
       g.t_off = (int)(off / 2);
       T = reinterpret_cast<uint16_t*>(blob + off);
       // layout [4 chunks][rows = halves x 32][8 uint16]: entry e of a row is in chunk e / 8
@@ -1969,6 +2048,56 @@ size_t build_block(const tanq_sim* s, const FusedOp& op, tanq::BlockParams& p, u
       off += (size_t)halves * 32 * 16 * 2;
     }
   }
+  p.rb_nq = 0;
+  p.rb_off = 0;
+  if (rb) {  // transform tables: [qubit][64 pair threads][4 pairs][x1 slot, x2 slot]
+    p.rb_off = (int)(off / 2);
+    uint16_t* RT = reinterpret_cast<uint16_t*>(blob + off);
+    for (int j = 0; j < op.k; ++j) {
+      const int rbit = bit_of_pos((int)s->phys[2 * op.q[j]]);
+      const int cbit = bit_of_pos((int)s->phys[2 * op.q[j] + 1]);
+      std::vector<int> ob;
+      for (int b = 0; b < 10; ++b)
+        if (b != rbit && b != cbit) ob.push_back(b);
+      // the 3 lane bits of a quarter warp: the triple spreading x1 and x2 over the most banks
+      std::vector<int> best_ob = ob;
+      int best = 1 << 30;
+      for (int x = 0; x < 8; ++x)
+        for (int y = x + 1; y < 8; ++y)
+          for (int z = y + 1; z < 8; ++z) {
+            std::vector<int> cand{ob[x], ob[y], ob[z]};
+            for (int u = 0; u < 8; ++u)
+              if (u != x && u != y && u != z) cand.push_back(ob[u]);
+            int cost = 0;
+            for (int hi = 0; hi < 32; ++hi)
+              for (int which = 0; which < 2; ++which) {
+                int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, m = 0;
+                for (int l = 0; l < 8; ++l) {
+                  int idx = 1 << (which ? cbit : rbit);
+                  const int o = l | (hi << 3);
+                  for (int b = 0; b < 8; ++b)
+                    if ((o >> b) & 1) idx |= 1 << cand[b];
+                  m = std::max(m, ++cnt[slot(idx) & 7]);
+                }
+                cost += m;
+              }
+            if (cost < best) {
+              best = cost;
+              best_ob = cand;
+            }
+          }
+      for (int o = 0; o < 256; ++o) {
+        int base = 0;
+        for (int b = 0; b < 8; ++b)
+          if ((o >> b) & 1) base |= 1 << best_ob[b];
+        const int pt = o & 63, jj = o >> 6;
+        RT[((size_t)(j * 64 + pt) * 4 + jj) * 2 + 0] = (uint16_t)slot(base | (1 << rbit));
+        RT[((size_t)(j * 64 + pt) * 4 + jj) * 2 + 1] = (uint16_t)slot(base | (1 << cbit));
+      }
+    }
+    p.rb_nq = op.k;
+    off += (size_t)op.k * 64 * 8 * 2;
+  }
   if (use_tma) {  // slot table for the cp.async path of blocks that are not moved by TMA
     p.slot_off = (int)(off / 2);
     uint16_t* st = reinterpret_cast<uint16_t*>(blob + off);
@@ -2009,12 +2138,15 @@ tanq_status launch_op(tanq_sim* s, const FusedOp& op, const tanq::GroupParams* g
   const double amps = (double)((uint64_t)1 << s->L);
   // algorithmic: 8 flops per complex MAC; executed: K1 (FMA) 8, K2 / K3 (3-multiply DMMA) 6
   double flops_amp = 8.0 * M, hw_amp = (k == 1 ? 8.0 : 6.0) * M;
+  // (real basis: k=2 sub-ops execute 4 -- two real products)
+  const double hw2 = (bp && bp->rb_nq) ? 4.0 : 6.0;
+  if (bp && op.sub.empty() && k == 2) hw_amp = hw2 * M;
   if ((gp || bp) && !op.sub.empty()) {
     flops_amp = hw_amp = 0;
     for (const auto& sb : op.sub) {
       const int Ms = 1 << (2 * sb.k);
       flops_amp += 8.0 * Ms;
-      hw_amp += (sb.k == 1 ? 8.0 : 6.0) * Ms;
+      hw_amp += (sb.k == 1 ? 8.0 : hw2) * Ms;
     }
   }
   const bool mir_op = gp ? gp->mirror != 0 : (bp ? bp->mirror != 0 : use_mirror(s, op));

@@ -98,6 +98,14 @@ struct BlockParams {
   int32_t tbox[5];
   int32_t hi_blk;            // highest block bit position
   int32_t slot_off;          // uint16 offset of the 1024-entry slot table in the blob
+  // Real basis (rb_nq > 0): after the load the block is transformed on rb_nq
+  // group qubits -- each qubit's (row 1 col 0, row 0 col 1) element pair (x1, x2) becomes
+  // (x1 + x2, i (x2 - x1)) -- where every Hermiticity-preserving sub-op is a REAL matrix R:
+  // k=2 sub-ops run as 2 real DMMA products (R Re x, R Im x; fragments [4 ks][32][2 mt])
+  // instead of 3; the inverse transform runs before the store.  Tables at rb_off (uint16):
+  // [rb_nq][64 pair threads][4 pairs][2 slots].
+  int32_t rb_nq;
+  int32_t rb_off;
 };
 
 // Transpose descriptor of a shard in the packed Hermitian layout.  The

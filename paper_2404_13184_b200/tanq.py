@@ -94,7 +94,8 @@ class tanq_block_params(ctypes.Structure):
                 ("start_by_pidx", ctypes.c_uint16 * 64), ("sub", tanq_block_sub * 12),
                 ("tma", ctypes.c_uint32), ("tdims", ctypes.c_int32), ("tlo", ctypes.c_int32 * 5),
                 ("tbits", ctypes.c_int32 * 5), ("tbox", ctypes.c_int32 * 5),
-                ("hi_blk", ctypes.c_int32), ("slot_off", ctypes.c_int32)]
+                ("hi_blk", ctypes.c_int32), ("slot_off", ctypes.c_int32),
+                ("rb_nq", ctypes.c_int32), ("rb_off", ctypes.c_int32)]
 
 
 class tanq_info(ctypes.Structure):

@@ -31,7 +31,7 @@ def compute():
         for world in (1, 2, 4, 8):
             if 2 * n - (world.bit_length() - 1) < 8:
                 continue
-            for fuse, kmax in ((2, 3), (2, 4)):
+            for fuse, kmax in ((2, 3), (2, 4), (2, 5)):
                 info = Plan(None, c, nm, fuse=fuse, k_max=kmax, world_size=world).info()
                 table[key(config, n, world, fuse, kmax)] = {
                     "gates": len(c.ops), "gate_updates": info["gate_updates"],

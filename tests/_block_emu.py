@@ -99,6 +99,15 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                 idm = pswap_bits(idx, 10)
                 if idx > idm:
                     st[slot(idx)] = np.conj(st[slot(idm)])
+        rb_nq = int(getattr(prm, "rb_nq", 0))
+        if rb_nq:   # real basis: forward transform of each group qubit's (10, 01) pairs
+            RT = u16[int(prm.rb_off):int(prm.rb_off) + rb_nq * 512].reshape(rb_nq, 256, 2)
+            for t in range(rb_nq):
+                if check:
+                    assert len(set(RT[t].reshape(-1).tolist())) == 512
+                for o1, o2 in RT[t]:
+                    x1, x2 = st[o1], st[o2]
+                    st[o1], st[o2] = x1 + x2, 1j * (x2 - x1)
         for q in range(int(prm.n_sub)):
             g = prm.sub[q]
             for h in range(2):
@@ -127,14 +136,19 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                     if check:   # the inputs are members of the lane's own 16-member tuple
                         assert len(set(wr)) == 512 and set(rd) <= set(wr)
                 elif g.k == 2:
-                    F = dbl[g.a_off:g.a_off + 768].reshape(3, 4, 32, 2).transpose(0, 3, 1, 2)
-                    a_ = F[0]
-                    b_ = F[2] + F[0]
-                    if check:
+                    if rb_nq:   # real fragments [4 ks][32 lanes][2 mt]: R only
+                        a_ = dbl[g.a_off:g.a_off + 256].reshape(4, 32, 2).transpose(2, 0, 1)
+                        b_ = np.zeros_like(a_)
+                        F = None
+                    else:
+                        F = dbl[g.a_off:g.a_off + 768].reshape(3, 4, 32, 2).transpose(0, 3, 1, 2)
+                        a_ = F[0]
+                        b_ = F[2] + F[0]
+                    if check and F is not None:
                         assert np.allclose(F[1], -(a_ + b_), atol=1e-14, rtol=1e-14)
                         for mt in range(2):       # tiles the kernel skips are exactly zero
                             for ks in range(4):
-                                if not (int(g.tmask) >> (mt * 4 + ks)) & 1:
+                                if not (int(g.tmask) >> (mt * 4 + ks)) & 1 and F is not None:
                                     assert not F[:, mt, ks, :].any(), (q, mt, ks)
                     S = np.zeros((16, 16), dtype=np.complex128)
                     X = np.zeros((16, 32), dtype=np.complex128)
@@ -172,6 +186,11 @@ def emulate(a: np.ndarray, prm, blob: np.ndarray, check=True):
                             st[offs] = S @ st[offs]
                     if check:
                         assert len(set(rd)) == 512
+        if rb_nq:   # backward transform before the stores
+            for t in range(rb_nq):
+                for o1, o2 in RT[t]:
+                    u1, u2 = st[o1], st[o2]
+                    st[o1], st[o2] = (u1 + 1j * u2) / 2, (u1 - 1j * u2) / 2
         for j in range(64):
             tr, src, pidx = trs[j]
             for t in range(16):

@@ -1567,14 +1567,17 @@ BlockSubChoice best_choice(int k, const std::vector<int>& mem, const std::vector
 // which J-invariant vectors have real coordinates -- per qubit e00, e10 + e01, i (e01 - e10),
 // e11 -- it is a real matrix R = F S F^-1.  Groups whose sub-ops are all Hermiticity-preserving
 // transform the block once after the load and back before the store; every k=2 sub-op then
-// needs 2 real DMMA products instead of 3.  Env TANQ_RBASIS=0 disables; groups with fewer
-// than TANQ_RBASIS_MIN (default 1) k=2 sub-ops stay complex.
+// needs 2 real DMMA products instead of 3.  Opt-in (env TANQ_RBASIS=1; TANQ_RBASIS_MIN = the
+// fewest k=2 sub-ops a group needs, default 1): measured slower on B200 -- QPE-16 113.4 vs
+// 127.1 updates/s, config 3 (k_max 4) 1751 vs 1842 (profiles/r02_rbasis_experiment.txt): the
+// per-qubit pair passes over shared memory and their pair barriers cost more than the third
+// of the DMMAs they save.
 int rbasis_min() {
   static int v = -2;
   if (v == -2) {
     const char* e = std::getenv("TANQ_RBASIS");
     const char* m = std::getenv("TANQ_RBASIS_MIN");
-    v = (e && e[0] == '0') ? -1 : (m ? std::max(1, std::atoi(m)) : 1);
+    v = !(e && e[0] == '1') ? -1 : (m ? std::max(1, std::atoi(m)) : 1);
   }
   return v;
 }

@@ -6,6 +6,8 @@ fragment permutations) and the result must equal the plan op's superoperator app
 CPU oracle.  Also checks that the shared-memory placement makes the DMMA fragment accesses of
 3-qubit groups above qubit 1 bank-conflict free (8 distinct 16 B banks per quarter warp).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -292,3 +294,20 @@ def test_block_groups_kmax5_circuit(Plan, case, packed):
     ref = dense.run(c, nm)
     assert np.abs(got - ref).max() < 1e-12
     assert syncs > 0   # some block group changed its warp-half bit between sub-ops
+
+
+@pytest.mark.skipif(os.environ.get("TANQ_RBASIS") == "1", reason="nested run")
+def test_block_programs_real_basis():
+    """TANQ_RBASIS=1 (opt-in, read once per process: a nested pytest run): every group whose
+    sub-ops preserve Hermiticity is transformed to the real basis (per-qubit pair tables,
+    real R fragments, inverse transform before the store); the emulated programs must still
+    equal the oracle, per op and over whole k_max = 5 plans."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TANQ_RBASIS="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", os.path.abspath(__file__),
+                        "-k", "emulation_matches_oracle or kmax5 or four_qubit or standalone"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

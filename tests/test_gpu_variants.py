@@ -61,15 +61,18 @@ print("OK", worst)
     ("warp", "direct", "1", "0"), ("q1", "tile", "1", "0"), ("o1", "auto", "1", "0"),
     ("auto", "auto", "1", "0"), ("auto", "direct", "0", "0"), ("q1", "auto", "0", "0"),
     ("warp", "tile", "0", "0"), ("o1", "tile", "0", "0"),
-    ("auto", "auto", "1", "64"), ("auto", "auto", "0", "64")])
+    ("auto", "auto", "1", "64"), ("auto", "auto", "0", "64"),
+    ("auto", "auto", "1", "rb"), ("auto", "auto", "0", "rb")])
 def test_kernel_variant_parity(group, k2path, mirror, sparse):
     """sparse = 64: the block kernel's sparse DFMA sub-op (TANQ_SPARSE_MAX) for every k=2
-    sub-op with at most 64 nonzeros."""
+    sub-op with at most 64 nonzeros; sparse = rb: the real-basis block programs
+    (TANQ_RBASIS=1)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ, TANQ_GROUP=group, TANQ_K2PATH=k2path, TANQ_MIRROR=mirror,
-               TANQ_SPARSE_MAX=sparse)
+               TANQ_SPARSE_MAX="0" if sparse == "rb" else sparse,
+               TANQ_RBASIS="1" if sparse == "rb" else "0")
     r = subprocess.run([sys.executable, "-c", SNIPPET % {"root": ROOT}], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]

@@ -53,6 +53,13 @@ __device__ __forceinline__ uint64_t tpose64(uint64_t x, uint64_t lo, uint64_t m,
   const uint64_t l = lo >> r;
   return pair_swap64(x & l) | ((x & ~l) ^ (m >> r));
 }
+// MODE bit 1: the shard's transpose descriptor (several shards, parity layout); without it
+// the single-shard pair_swap (the same map for tp_lo = ~0, tp_m = 0).
+template <int MODE>
+__device__ __forceinline__ uint64_t tpb(uint64_t x, const BlockParams& p, int r) {
+  if constexpr ((MODE & 2) != 0) return tpose64(x, p.tp_lo, p.tp_m, r);
+  else return pair_swap64(x);
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -483,7 +490,7 @@ static_assert(16 * kBlockMaxPairs + 64 * 8 + 64 * 2 <= kBlockHdrBytes, "block he
 // cp.async.cg copies (16 per thread, 16 lanes per piece: every warp instruction reads two
 // contiguous 256 B runs), signalled with cp.async.mbarrier.arrive, and store it back with
 // coalesced LDS + STG.128 -- no per-lane serialised bulk-copy issue.
-template <int UI, int COPY, int ACC>
+template <int UI, int COPY, int ACC, int MODE>
 __global__ void __launch_bounds__(384, 1)
     block_kernel(double2* __restrict__ a, const __grid_constant__ BlockParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -518,19 +525,19 @@ __global__ void __launch_bounds__(384, 1)
   const bool mirror = p.mirror != 0;
   auto next_block = [&](uint64_t i) {
     if (mirror)
-      while (i < nb && i > tpose64(i, p.tp_lo, p.tp_m, 10)) i += npairs;
+      while (i < nb && i > tpb<MODE>(i, p, 10)) i += npairs;
     return i;
   };
   // where piece (offset go) of the block at `base` lives: in place, or (packed layout,
   // non-canonical piece of a block that is not self-transposed) at the transposed position
   auto piece_src = [&](uint64_t base, bool self, uint64_t go, bool& tr) {
     const uint64_t e0 = base + go;
-    const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
+    const uint64_t em = tpb<MODE>(e0, p, 0);
     tr = mirror && !self && e0 > em;
     return tr ? em : e0;
   };
   auto is_self = [&](uint64_t base) {
-    return mirror && tpose64(base, p.tp_lo, p.tp_m, 0) == base;
+    return mirror && tpb<MODE>(base, p, 0) == base;
   };
   auto issue = [&](uint64_t i, int s) {
     uint64_t* bar = &mbar[pair * 2 + s];
@@ -600,27 +607,43 @@ __global__ void __launch_bounds__(384, 1)
       if (!first && nxt < nb) issue(nxt, s ^ 1);
     }
     if (!(p.dbg & 1)) {
-      const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
-      blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
-      for (int q = 0; q < p.n_sub; ++q) {
-        const BlockSub& g = p.sub[q];
-        if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
-        const bool shared_tab = g.hadd >= 0;
-        double2* Xh = X + (shared_tab ? half * g.hadd : 0);
+      if constexpr ((MODE & 1) != 0) {  // sparse / real-basis / per-sub-op split programs
+        const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
+        blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
+        for (int q = 0; q < p.n_sub; ++q) {
+          const BlockSub& g = p.sub[q];
+          if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
+          const bool shared_tab = g.hadd >= 0;
+          double2* Xh = X + (shared_tab ? half * g.hadd : 0);
+          const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
+          const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+          const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
+          if (g.k == 2 && g.nnz)
+            blk_sub_k2s(Xh, F, T, trow, trows, g.nnz);
+          else if (g.k == 2 && p.rb_nq)
+            blk_sub_k2r(Xh, F, T, lane, trow, trows);
+          else if (g.k == 2)
+            blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
+          else
+            blk_sub_k1(Xh, F, T, trow, trows);
+          __syncwarp();
+        }
+        blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
+      } else {
+        const bool shared_tab = p.half_add >= 0;
+        double2* Xh = X + (shared_tab ? half * p.half_add : 0);
         const int trow = shared_tab ? lane : half * 32 + lane, trows = shared_tab ? 32 : 64;
-        const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
-        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
-        if (g.k == 2 && g.nnz)
-          blk_sub_k2s(Xh, F, T, trow, trows, g.nnz);
-        else if (g.k == 2 && p.rb_nq)
-          blk_sub_k2r(Xh, F, T, lane, trow, trows);
-        else if (g.k == 2)
-          blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
-        else
-          blk_sub_k1(Xh, F, T, trow, trows);
-        __syncwarp();
+        for (int q = 0; q < p.n_sub; ++q) {
+          const BlockSub& g = p.sub[q];
+          const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+          const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
+          if (g.k == 2)
+            blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, trows);
+          else
+            blk_sub_k1(Xh, F, T, trow, trows);
+          __syncwarp();
+        }
       }
-      blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
     }
     pair_bar(pair);
     if (trp) piece_transpose(X + sstart, rot);
@@ -659,7 +682,7 @@ __global__ void __launch_bounds__(384, 1)
 //   otherwise -- every pair thread issues 16 cp.async 16 B copies (16 lanes per 256 B piece)
 //   straight to each element's final slot (pieces read from the transposed position land
 //   already permuted), conjugates them after the wait, and stores them back with STG.
-template <int UI, int ACC>
+template <int UI, int ACC, int MODE>
 __global__ void __launch_bounds__(384, 1)
     block_kernel_tma(double2* __restrict__ a, const __grid_constant__ BlockParams p,
                      const __grid_constant__ CUtensorMap tmap) {
@@ -686,14 +709,14 @@ __global__ void __launch_bounds__(384, 1)
   const bool mirror = p.mirror != 0;
   auto next_block = [&](uint64_t i) {
     if (mirror)
-      while (i < nb && i > tpose64(i, p.tp_lo, p.tp_m, 10)) i += npairs;
+      while (i < nb && i > tpb<MODE>(i, p, 10)) i += npairs;
     return i;
   };
   // block classification: 0 direct (TMA), 1 cp.async with transposed pieces, 2 self-transposed
   auto kind_of = [&](uint64_t base) {
     if (!mirror) return 0;
-    const uint64_t d =
-        (base ^ tpose64(base, p.tp_lo, p.tp_m, 0)) & (0x5555555555555555ull | ~p.tp_lo);
+    const uint64_t d = (base ^ tpb<MODE>(base, p, 0)) &
+                       (0x5555555555555555ull | ((MODE & 2) != 0 ? ~p.tp_lo : 0ull));
     if (!d) return 2;
     return (63 - __clzll(d)) > p.hi_blk ? 0 : 1;
   };
@@ -727,7 +750,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int it = 0; it < 16; ++it) {
         const int q = it * 4 + qb;
         const uint64_t e0 = base + p.piece_goff[q];
-        const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
+        const uint64_t em = tpb<MODE>(e0, p, 0);
         const bool tr = kd == 1 && e0 > em;
         cp_async16_cg(st + sSlot[q * 16 + (tr ? pswap4(u) : u)], a + (tr ? em : e0) + u);
       }
@@ -754,7 +777,7 @@ __global__ void __launch_bounds__(384, 1)
     const int kd = (p.dbg & 2) ? 0 : kind_of(base);
     if (kd == 1) {  // conjugate the pieces that came from the transposed position
       const uint64_t e0 = base + p.piece_goff[pt];
-      if (e0 > tpose64(e0, p.tp_lo, p.tp_m, 0)) {
+      if (e0 > tpb<MODE>(e0, p, 0)) {
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           double* im = &X[sSlot[pt * 16 + ((t + pt) & 15)]].y;
@@ -774,26 +797,40 @@ __global__ void __launch_bounds__(384, 1)
     pair_bar(pair);
     if (!first && nxt < nb) issue(nxt, s ^ 1);
     if (!(p.dbg & 1)) {
-      double2* Xh = X;
-      const int trow = half * 32 + lane;
-      const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
-      blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
-      for (int q = 0; q < p.n_sub; ++q) {
-        const BlockSub& g = p.sub[q];
-        if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
-        const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
-        const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
-        if (g.k == 2 && g.nnz)
-          blk_sub_k2s(Xh, F, T, trow, 64, g.nnz);
-        else if (g.k == 2 && p.rb_nq)
-          blk_sub_k2r(Xh, F, T, lane, trow, 64);
-        else if (g.k == 2)
-          blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, 64);
-        else
-          blk_sub_k1(Xh, F, T, trow, 64);
-        __syncwarp();
+      if constexpr ((MODE & 1) != 0) {  // sparse / real-basis / per-sub-op split programs
+        double2* Xh = X;
+        const int trow = half * 32 + lane;
+        const uint16_t* RB = reinterpret_cast<const uint16_t*>(sBlob) + p.rb_off;
+        blk_rbasis(X, RB, p.rb_nq, pt, pair, true);
+        for (int q = 0; q < p.n_sub; ++q) {
+          const BlockSub& g = p.sub[q];
+          if (g.sync) pair_bar(pair);  // the other warp's half of the last sub-op is done
+          const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+          const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
+          if (g.k == 2 && g.nnz)
+            blk_sub_k2s(Xh, F, T, trow, 64, g.nnz);
+          else if (g.k == 2 && p.rb_nq)
+            blk_sub_k2r(Xh, F, T, lane, trow, 64);
+          else if (g.k == 2)
+            blk_sub_k2<UI, ACC>(Xh, F, T, lane, trow, 64);
+          else
+            blk_sub_k1(Xh, F, T, trow, 64);
+          __syncwarp();
+        }
+        blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
+      } else {
+        const int trow = half * 32 + lane;
+        for (int q = 0; q < p.n_sub; ++q) {
+          const BlockSub& g = p.sub[q];
+          const double* F = reinterpret_cast<const double*>(sBlob) + g.a_off;
+          const uint16_t* T = reinterpret_cast<const uint16_t*>(sBlob) + g.t_off;
+          if (g.k == 2)
+            blk_sub_k2<UI, ACC>(X, F, T, lane, trow, 64);
+          else
+            blk_sub_k1(X, F, T, trow, 64);
+          __syncwarp();
+        }
       }
-      blk_rbasis(X, RB, p.rb_nq, pt, pair, false);
     }
     if (kd == 0) fence_async_smem();
     pair_bar(pair);
@@ -811,7 +848,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int it = 0; it < 16; ++it) {
           const int q = it * 4 + qb;
           const uint64_t e0 = base + p.piece_goff[q];
-          const uint64_t em = tpose64(e0, p.tp_lo, p.tp_m, 0);
+          const uint64_t em = tpb<MODE>(e0, p, 0);
           const bool tr = kd == 1 && e0 > em;
           double2 v = X[sSlot[q * 16 + (tr ? pswap4(u) : u)]];
           if (tr) v.y = -v.y;
@@ -862,10 +899,10 @@ static cudaError_t encode_block_tmap(CUtensorMap* map, double2* a, const BlockPa
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int ACC>
+template <int ACC, int MODE>
 static cudaError_t launch_block_tma(double2* a, const BlockParams& p, cudaStream_t st) {
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = block_kernel_tma<2, ACC>;
+  auto kern = block_kernel_tma<2, ACC, MODE>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -894,11 +931,11 @@ static cudaError_t launch_block_tma(double2* a, const BlockParams& p, cudaStream
   return cudaGetLastError();
 }
 
-template <int UI, int COPY, int ACC>
+template <int UI, int COPY, int ACC, int MODE>
 static cudaError_t launch_block_cfg(double2* a, const BlockParams& p, size_t smem,
                                     cudaStream_t st) {
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = block_kernel<UI, COPY, ACC>;
+  auto kern = block_kernel<UI, COPY, ACC, MODE>;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -938,18 +975,38 @@ cudaError_t launch_block_group(double2* a, const BlockParams& p, int L, cudaStre
     const char* f = getenv("TANQ_BLOCK_ACC");
     acc = (f && f[0] == '1') ? 1 : ((f && f[0] == '2') ? 2 : 0);
   }
-  if (p.tma) return acc == 2 ? launch_block_tma<2>(a, p, st) : launch_block_tma<0>(a, p, st);
+  // MODE: bit 0 = the program uses sparse / real-basis / per-sub-op-split sub-ops, bit 1 = a
+  // non-trivial shard transpose descriptor; the plain single-shard programs of the bench run
+  // the instantiation without either (their extra code measurably slowed the hot loop)
+  bool ext = p.rb_nq > 0;
+  for (int q = 0; q < p.n_sub; ++q)
+    ext = ext || p.sub[q].nnz > 0 || p.sub[q].sync != 0 || p.sub[q].hadd != p.half_add;
+  const int mode = (ext ? 1 : 0) | ((p.tp_lo != ~0ull || p.tp_m != 0) ? 2 : 0);
+  if (p.tma) {
+    if (acc == 2) return launch_block_tma<2, 3>(a, p, st);
+    switch (mode) {
+      case 0: return launch_block_tma<0, 0>(a, p, st);
+      case 1: return launch_block_tma<0, 1>(a, p, st);
+      case 2: return launch_block_tma<0, 2>(a, p, st);
+      default: return launch_block_tma<0, 3>(a, p, st);
+    }
+  }
   const size_t smem = block_smem_bytes(p.pairs, p.blob_bytes);
   if (smem > 227 * 1024 || p.pairs < 1 || p.pairs > kBlockMaxPairs) return cudaErrorInvalidValue;
-  if (acc == 1) {
-    if (copy == 1) return launch_block_cfg<2, 1, 1>(a, p, smem, st);
-    if (copy == 2) return launch_block_cfg<2, 2, 1>(a, p, smem, st);
-    return launch_block_cfg<2, 0, 1>(a, p, smem, st);
+  if (acc == 1) {  // experiment variants: the generic instantiation
+    if (copy == 1) return launch_block_cfg<2, 1, 1, 3>(a, p, smem, st);
+    if (copy == 2) return launch_block_cfg<2, 2, 1, 3>(a, p, smem, st);
+    return launch_block_cfg<2, 0, 1, 3>(a, p, smem, st);
   }
-  if (acc == 2) return launch_block_cfg<2, 0, 2>(a, p, smem, st);
-  if (copy == 1) return launch_block_cfg<2, 1, 0>(a, p, smem, st);
-  if (copy == 2) return launch_block_cfg<2, 2, 0>(a, p, smem, st);
-  return launch_block_cfg<2, 0, 0>(a, p, smem, st);
+  if (acc == 2) return launch_block_cfg<2, 0, 2, 3>(a, p, smem, st);
+  if (copy == 1) return launch_block_cfg<2, 1, 0, 3>(a, p, smem, st);
+  if (copy == 2) return launch_block_cfg<2, 2, 0, 3>(a, p, smem, st);
+  switch (mode) {
+    case 0: return launch_block_cfg<2, 0, 0, 0>(a, p, smem, st);
+    case 1: return launch_block_cfg<2, 0, 0, 1>(a, p, smem, st);
+    case 2: return launch_block_cfg<2, 0, 0, 2>(a, p, smem, st);
+    default: return launch_block_cfg<2, 0, 0, 3>(a, p, smem, st);
+  }
 }
 
 }  // namespace tanq

@@ -2924,6 +2924,11 @@ tanq_status exec_graph(tanq_sim* s, const tanq_plan* p) {
                    g.mirror == s->mirror_allowed && g.packed == s->packed &&
                    std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0;
   CUDA_TRY(cudaSetDevice(sh.device));
+  if (const char* e = std::getenv("TANQ_GRAPH_DEBUG"); e && e[0] == '1')
+    std::fprintf(stderr, "exec_graph: %s (exec %d sim %d data %d herm %d mirror %d packed %d phys %d)\n",
+                 hit ? "replay" : "capture", g.exec != nullptr, g.sim == s, g.data == sh.data,
+                 g.herm == s->herm_state, g.mirror == s->mirror_allowed, g.packed == s->packed,
+                 std::memcmp(g.phys, s->phys, sizeof(g.phys)) == 0);
   if (!hit) {
     if (g.exec) {
       CUDA_TRY(cudaGraphExecDestroy(g.exec));

@@ -176,7 +176,8 @@ def _worker(rank, world, port, n, seed, out_path, layout):
 
 @pytest.mark.parametrize("world,n,seed,layout", [
     (2, 4, 1, "bits"), (2, 5, 2, "bits"), (4, 5, 3, "bits"), (4, 4, 4, "bits"),
-    (2, 6, 5, "parity"), (2, 7, 6, "parity"), (4, 7, 7, "parity"), (4, 8, 8, "parity")])
+    (2, 6, 5, "parity"), (2, 7, 6, "parity"), (4, 7, 7, "parity"), (4, 8, 8, "parity"),
+    (8, 8, 9, "parity")])
 def test_distributed_schedule_matches_oracle(tmp_path, world, n, seed, layout):
     import torch.multiprocessing as mp
     from oracle import dense

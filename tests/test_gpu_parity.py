@@ -162,7 +162,8 @@ def test_virtual_shards_remap(Sim, shards, seed):
 
 
 @pytest.mark.parametrize("n,shards,kmax,seed", [
-    (8, 2, 3, 0), (8, 4, 3, 1), (9, 8, 3, 2), (9, 2, 4, 3), (10, 4, 3, 4), (10, 2, 2, 5)])
+    (8, 2, 3, 0), (8, 4, 3, 1), (9, 8, 3, 2), (9, 2, 4, 3), (10, 4, 3, 4), (10, 2, 2, 5),
+    (9, 2, 5, 6)])   # k_max 5: block groups run as their sub-ops on several shards
 def test_virtual_shards_parity_packed(Sim, n, shards, kmax, seed):
     """Shard-local parity layout: with >= 6 fully local qubits every shard runs
     the packed Hermitian kernels (per-shard transpose descriptor), remaps trade a half-global
